@@ -422,6 +422,111 @@ int nx_kv_page_log(const nx_engine* eng, char* buf, size_t cap, size_t* len);
 /* Page size (tokens) and pool size (pages); set before the first submit. */
 int nx_kv_configure(nx_engine* eng, int32_t page_tokens, int32_t num_pages);
 
+/* ---- device executor (new: the reference has no GPU path) ----
+ * The kernels that replace the analytic operators (opcost.hpp:22):
+ * QkvProj/AttnOutProj/Ffn -> tcgen05 GEMMs, AttnPrefill/AttnDecode -> paged
+ * attention kernels, plus RMSNorm/RoPE/embedding/lm_head+argmax. */
+
+/* Llama/Qwen-style decoder geometry (the reference's ModelConfig stays the
+ * cost-model view; this is the kernel view). head_dim must be 128; hidden,
+ * ffn and vocab multiples of 128. */
+typedef struct nx_arch {
+  int32_t hidden;
+  int32_t n_layers;
+  int32_t n_heads;
+  int32_t n_kv_heads;
+  int32_t head_dim;
+  int32_t ffn;
+  int32_t vocab;
+  int32_t qkv_bias; /* 1: QKV projection has a bias (Qwen2.5) */
+  float rope_theta;
+  float rms_eps;
+} nx_arch;
+
+typedef struct nx_device_config {
+  nx_arch arch;
+  int32_t device;             /* CUDA ordinal */
+  int32_t page_tokens;        /* KV page size in tokens (16) */
+  int32_t num_pages;          /* KV pool size in pages */
+  int32_t max_prefill_tokens; /* token budget (+ decode batch for mixed lanes) */
+  int32_t max_decode_batch;
+  int32_t green_contexts;     /* 1: partition SMs per lane with CUDA green contexts */
+  uint64_t weight_seed;
+  float weight_gain;   /* weights ~ U(+-gain * sqrt(3/K)) -> unit-variance outputs */
+  float lm_head_gain;  /* larger gain on lm_head widens the logit spread */
+} nx_device_config;
+
+typedef struct nx_device nx_device;
+
+typedef struct nx_device_info {
+  int32_t sm_count;
+  int32_t n_layouts;        /* green-context layouts (0 if disabled) */
+  int32_t layout_decode_sms[32];
+  int32_t layout_prefill_sms[32];
+  uint64_t weight_bytes;
+  uint64_t kv_bytes;
+  uint64_t workspace_bytes;
+} nx_device_info;
+
+/* Allocates weights (deterministic random init on device), the paged KV
+ * cache, per-lane workspaces, and pre-instantiates every green-context SM
+ * layout. NX_ENODEV without a usable sm_100 GPU. */
+int nx_device_create(const nx_device_config* cfg, nx_device** out);
+void nx_device_destroy(nx_device* dev);
+int nx_device_get_info(const nx_device* dev, nx_device_info* out);
+/* Binds a device to an engine (before submitting requests); every launched
+ * batch then runs on the device; tokens are greedy. */
+int nx_engine_bind_device(nx_engine* eng, nx_device* dev);
+
+/* Weight tensors, raw device layout (bf16). layer is ignored for global ones. */
+#define NX_W_EMBED 0
+#define NX_W_ATTN_NORM 1
+#define NX_W_QKV 2      /* [(H + 2 Hkv) hd, hidden] */
+#define NX_W_QKV_BIAS 3 /* [(H + 2 Hkv) hd] */
+#define NX_W_O 4        /* [hidden, H hd] */
+#define NX_W_FFN_NORM 5
+#define NX_W_GATE_UP 6 /* [2 ffn, hidden]; 128-row blocks = 64 gate rows then the 64 matching up rows */
+#define NX_W_DOWN 7    /* [hidden, ffn] */
+#define NX_W_FINAL_NORM 8
+#define NX_W_LM_HEAD 9 /* [vocab, hidden] */
+int nx_device_weight(const nx_device* dev, int32_t tensor, int32_t layer, void* host,
+                     size_t cap_bytes, size_t* bytes);
+
+/* One forward batch, synchronous (kernel-level tests and the bench). Members
+ * are described by parallel arrays; tokens holds sum(n_tokens) ids; pages
+ * holds each member's page list back to back (n_pages each). lane: 0 prefill
+ * / mixed lane, 1 decode lane; sm_pct picks the partition layout. Writes one
+ * sampled token per member with sample[i] != 0 and, if logits != NULL, their
+ * fp32 logits (row-major [n_sampled, vocab]). */
+typedef struct nx_batch_desc {
+  int32_t lane;
+  int32_t sm_pct;
+  int32_t n_members;
+  int32_t _pad0;
+  const int32_t* n_tokens;
+  const int64_t* start_pos;
+  const int32_t* sample;
+  const int32_t* tokens;
+  const int32_t* n_pages;
+  const int32_t* pages;
+} nx_batch_desc;
+int nx_device_forward(nx_device* dev, const nx_batch_desc* b, int32_t* sampled, float* logits,
+                      double* device_ms);
+
+/* ---- raw device plumbing + single-op entry points (tests / profiling) --- */
+int nx_dev_malloc(size_t bytes, void** p);
+int nx_dev_free(void* p);
+int nx_dev_h2d(void* dst, const void* src, size_t bytes);
+int nx_dev_d2h(void* dst, const void* src, size_t bytes);
+int nx_dev_sync(void);
+/* out = epilogue(x[tokens, K] . w[rows, K]^T) with the tcgen05 GEMM; mode is
+ * the epilogue (0 store, 1 bias, 2 residual, 3 bias+residual, 4 SwiGLU,
+ * 6 fp32). sm_count caps the persistent grid; splits 0 = automatic.
+ * Returns the device time of `iters` launches in *ms (may be NULL). */
+int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32_t K, int32_t mode,
+               void* out, int32_t ldo, const void* bias, const void* residual, int32_t ldr,
+               int32_t sm_count, int32_t splits, int32_t iters, float* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,186 @@
+// Device half of the C-ABI (include/nexus_b200.h, "device executor" section).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "capi_internal.hpp"
+#include "device.cuh"
+#include "model.cuh"
+
+struct nx_device {
+  std::unique_ptr<nxd::Model> m;
+};
+
+namespace {
+
+int dfail(int code, const std::string& what) {
+  nxb::last_error() = what;
+  return code;
+}
+
+template <class F>
+int dguard(F&& f) {
+  try {
+    nxb::last_error().clear();
+    return f();
+  } catch (const nxd::NoDevice& e) {
+    return dfail(NX_ENODEV, e.what());
+  } catch (const std::invalid_argument& e) {
+    return dfail(NX_EINVAL, e.what());
+  } catch (const std::bad_alloc&) {
+    return dfail(NX_ENOMEM, "out of memory");
+  } catch (const std::exception& e) {
+    return dfail(NX_ERUNTIME, e.what());
+  }
+}
+
+int cuda_rc(cudaError_t e) {
+  if (e == cudaSuccess) return NX_OK;
+  return dfail(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? NX_ENODEV : NX_ERUNTIME,
+               cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+int nx_device_create(const nx_device_config* cfg, nx_device** out) {
+  return dguard([&] {
+    auto d = std::make_unique<nx_device>();
+    d->m = std::make_unique<nxd::Model>(*cfg);
+    *out = d.release();
+    return NX_OK;
+  });
+}
+
+void nx_device_destroy(nx_device* dev) { delete dev; }
+
+int nx_device_get_info(const nx_device* dev, nx_device_info* out) {
+  std::memset(out, 0, sizeof(*out));
+  const nxd::Partitions& p = dev->m->partitions();
+  out->sm_count = p.total_sm;
+  out->n_layouts = static_cast<int32_t>(p.layouts.size());
+  for (size_t i = 0; i < p.layouts.size() && i < 32; ++i) {
+    out->layout_decode_sms[i] = p.layouts[i].decode_sms;
+    out->layout_prefill_sms[i] = p.layouts[i].prefill_sms;
+  }
+  out->weight_bytes = dev->m->weight_bytes();
+  out->kv_bytes = dev->m->kv_bytes();
+  return NX_OK;
+}
+
+int nx_engine_bind_device(nx_engine* eng, nx_device* dev) {
+  return dguard([&] {
+    eng->e.bind(dev->m.get(), /*owns=*/false);
+    return NX_OK;
+  });
+}
+
+int nx_device_weight(const nx_device* dev, int32_t tensor, int32_t layer, void* host,
+                     size_t cap_bytes, size_t* bytes) {
+  return dguard([&] {
+    size_t elems = 0;
+    const __nv_bfloat16* p = dev->m->weight_ptr(tensor, layer, &elems);
+    if (!p && elems) return dfail(NX_EINVAL, "unknown tensor/layer");
+    *bytes = elems * 2;
+    if (!host) return NX_OK;
+    if (cap_bytes < elems * 2) return dfail(NX_EINVAL, "buffer too small");
+    if (elems) {
+      const int rc = cuda_rc(cudaMemcpy(host, p, elems * 2, cudaMemcpyDeviceToHost));
+      if (rc) return rc;
+    }
+    return NX_OK;
+  });
+}
+
+int nx_device_forward(nx_device* dev, const nx_batch_desc* b, int32_t* sampled, float* logits,
+                      double* device_ms) {
+  return dguard([&] {
+    nxb::ExecBatch eb;
+    eb.lane_kind = b->lane == 1 ? NX_LANE_DECODE : NX_LANE_PREFILL;
+    eb.sm_pct = b->sm_pct;
+    size_t tok_off = 0, page_off = 0;
+    bool any_prefill = false, any_decode = false;
+    for (int i = 0; i < b->n_members; ++i) {
+      nxb::ExecMember m;
+      m.id = static_cast<uint64_t>(i);
+      m.n_tokens = b->n_tokens[i];
+      m.start_pos = b->start_pos[i];
+      m.sample = b->sample[i];
+      // Leading single-token members run through the decode kernel (same math).
+      m.is_prefill = (b->lane == 1 || (m.n_tokens == 1 && !any_prefill)) ? 0 : 1;
+      m.tokens = b->tokens + tok_off;
+      m.pages = b->pages + page_off;
+      m.n_pages = b->n_pages[i];
+      tok_off += m.n_tokens;
+      page_off += m.n_pages;
+      any_prefill |= m.is_prefill != 0;
+      any_decode |= m.is_prefill == 0;
+      eb.members.push_back(m);
+    }
+    if (b->lane == 0 && any_decode && any_prefill) eb.lane_kind = NX_LANE_MIXED;
+    const int slot = b->lane == 1 ? nxb::kLaneDecode : nxb::kLanePrefill;
+    dev->m->launch(slot, eb);
+    dev->m->wait(slot);
+    const std::vector<int32_t>& s = dev->m->sampled(slot);
+    if (sampled) std::memcpy(sampled, s.data(), s.size() * 4);
+    if (logits) dev->m->copy_logits(slot, logits, s.size() * static_cast<size_t>(dev->m->vocab()));
+    if (device_ms) *device_ms = dev->m->device_ms(slot);
+    return NX_OK;
+  });
+}
+
+int nx_dev_malloc(size_t bytes, void** p) { return cuda_rc(cudaMalloc(p, bytes)); }
+int nx_dev_free(void* p) { return cuda_rc(cudaFree(p)); }
+int nx_dev_h2d(void* dst, const void* src, size_t n) {
+  return cuda_rc(cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice));
+}
+int nx_dev_d2h(void* dst, const void* src, size_t n) {
+  return cuda_rc(cudaMemcpy(dst, src, n, cudaMemcpyDeviceToHost));
+}
+int nx_dev_sync(void) { return cuda_rc(cudaDeviceSynchronize()); }
+
+int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32_t K, int32_t mode,
+               void* out, int32_t ldo, const void* bias, const void* residual, int32_t ldr,
+               int32_t sm_count, int32_t splits, int32_t iters, float* ms) {
+  return dguard([&] {
+    const int bn = nxd::gemm_pick_bn(tokens);
+    CUtensorMap wm, xm;
+    if (!nxd::encode_kmajor(&wm, w, rows, K, static_cast<uint64_t>(K) * 2, 128) ||
+        !nxd::encode_kmajor(&xm, x, tokens, K, static_cast<uint64_t>(K) * 2, bn))
+      return dfail(NX_ERUNTIME, "tensor map encode failed");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int n_sm = 0;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (sm_count <= 0 || sm_count > n_sm) sm_count = n_sm;
+    float* ws = nullptr;
+    const size_t ws_bytes = 256u << 20;
+    int rc = cuda_rc(cudaMalloc(&ws, ws_bytes));
+    if (rc) return rc;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int n = iters > 0 ? iters : 1;
+    cudaError_t err = cudaSuccess;
+    cudaEventRecord(e0, nullptr);
+    for (int i = 0; i < n && err == cudaSuccess; ++i)
+      err = nxd::gemm(wm, xm, bn, rows, tokens, K, mode, out, ldo,
+                      static_cast<const __nv_bfloat16*>(bias),
+                      static_cast<const __nv_bfloat16*>(residual), ldr, ws, ws_bytes, sm_count,
+                      nullptr, splits);
+    cudaEventRecord(e1, nullptr);
+    if (err == cudaSuccess) err = cudaEventSynchronize(e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(ws);
+    return cuda_rc(err);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Internal device API of the B200 executor (kernels + launch helpers).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace nxd {
+
+// ---- GEMM (gemm_tc.cu) -------------------------------------------------------
+enum EpiMode {
+  kEpiStore = 0,         // out = acc (bf16)
+  kEpiBias = 1,          // out = acc + bias
+  kEpiResidual = 2,      // out = acc + residual (may alias out)
+  kEpiBiasResidual = 3,  // out = acc + bias + residual
+  kEpiSwiGLU = 4,        // out[f] = silu(acc[gate f]) * acc[up f]  (interleaved 64-row blocks)
+  kEpiPartial = 5,       // internal: fp32 K-split partials
+  kEpiF32 = 6,           // out = acc (fp32), e.g. logits
+};
+
+struct GemmParams {
+  int rows, tokens, K;
+  int n_mblk, n_nblk, splits, kb_per_split, num_kb;
+  int mode;
+  void* out;
+  int ldo;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* residual;
+  int ldr;
+  float* ws;
+};
+
+int gemm_pick_bn(int tokens);
+// y[tokens, rows] = epi(x[tokens, K] . w[rows, K]^T). `x_map` must have been
+// encoded with box rows == bn. sm_count sizes the persistent grid (the lane's
+// green-context partition); force_splits > 0 overrides the K-split choice.
+cudaError_t gemm(const CUtensorMap& w_map, const CUtensorMap& x_map, int bn, int rows, int tokens,
+                 int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
+                 const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
+                 cudaStream_t stream, int force_splits = 0);
+
+// K-major bf16 [rows, cols] tensor map with a 64 x box_rows, 128B-swizzled box.
+bool encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t row_stride_bytes, uint32_t box_rows);
+
+// ---- attention (attention.cu) ----------------------------------------------
+struct AttnGeom {
+  int n_heads, n_kv_heads, group, head_dim;
+  int page_tokens;
+  int qkv_stride;  // elements per token row of the qkv buffer
+  int out_stride;  // elements per token row of the attention output
+  float scale_log2;
+};
+
+struct AttnSeq {
+  int q_start;   // first row of this sequence in the batch
+  int q_len;     // new tokens this launch
+  int kv_len;    // keys after this launch (start + q_len)
+  int page_off;  // offset of the sequence's page list in the batch page array
+};
+
+size_t attn_smem_bytes();
+// work[i] = {sequence index, first query row} of 64-row blocks.
+cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
+                              const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
+                              const AttnSeq* seqs, const int2* work, int n_work,
+                              const int32_t* pages, __nv_bfloat16* out, cudaStream_t s);
+cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
+                             const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
+                             const AttnSeq* seqs, int n_seq, int max_kv_len, const int32_t* pages,
+                             __nv_bfloat16* out, float* part_o, float* part_ml, size_t part_cap,
+                             int sm_count, cudaStream_t s);
+
+// ---- elementwise / norm / sampling (kernels.cu) ----------------------------
+cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int hidden,
+                  __nv_bfloat16* out, cudaStream_t s);
+// out[r] = x[rows ? rows[r] : r] * rsqrt(mean(x^2) + eps) * w
+cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows, int n, int hidden,
+                    const __nv_bfloat16* w, float eps, __nv_bfloat16* out, cudaStream_t s);
+// Rotary embedding on q and k (rotate-half pairs), then k, v -> paged cache.
+cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* pos,
+                          const int32_t* slot, const float* inv_freq, int n_heads, int n_kv_heads,
+                          int head_dim, int page_tokens, __nv_bfloat16* kplane,
+                          __nv_bfloat16* vplane, cudaStream_t s);
+// out[r] = argmax_j logits[r, j] (lowest index on ties)
+cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, cudaStream_t s);
+// Deterministic random bf16 fill: uniform(-scale, scale) + offset from a hash of (seed, i).
+cudaError_t fill_random(__nv_bfloat16* p, size_t n, uint64_t seed, float scale, float offset,
+                        cudaStream_t s);
+
+}  // namespace nxd

@@ -1,0 +1,396 @@
+// Dense projection GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+//   out[t, f] = epilogue( sum_k X[t, k] * W[f, k] )      (y = x W^T)
+//
+// "Swap-AB" tiling: the weight tile is the MMA's A operand (M = 128 output
+// features) and the token tile is B (N = BN tokens), so one kernel serves
+// both the 2048-token prefill chunk (BN = 256, tensor-bound) and the
+// <= 64-token decode batch (BN = 32/64, HBM-bound on the weight stream:
+// every weight byte is read exactly once per launch).
+//
+// Structure (one CTA per SM, persistent over work units):
+//   warp 0      TMA producer: W and X 128B-swizzled K-major tiles -> smem ring
+//   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M128 x N x K16)
+//               into a double-buffered TMEM accumulator; owns TMEM alloc
+//   warps 2-5   epilogue: tcgen05.ld -> smem stage -> fused op -> coalesced
+//               16-byte global stores (bias / residual add / SwiGLU / fp32)
+// A work unit is (feature block, token block, K split). K splits > 1 write
+// fp32 partials that nxd_splitk_reduce() folds with the same epilogue; the
+// host picks splits so decode launches fill the lane's SM partition.
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "device.cuh"
+#include "ptx.cuh"
+
+namespace nxd {
+
+namespace {
+
+constexpr int kBM = 128;          // output features per tile (MMA M)
+constexpr int kBK = 64;           // K per stage: 64 bf16 = one 128B swizzle row
+constexpr int kThreads = 192;     // 6 warps
+constexpr int kEpiThreads = 128;
+constexpr int kABytes = kBM * kBK * 2;
+
+template <int BN>
+struct Cfg {
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStages = BN >= 256 ? 4 : BN >= 128 ? 5 : BN >= 64 ? 8 : 9;
+  static constexpr int kEpiBytes = 32 * kBM * 4;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int kSmem = 1024 + kStages * kStage + kEpiBytes + 256;
+};
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+struct Unit {
+  int m_blk, n_blk, split;
+};
+
+__device__ __forceinline__ Unit unit_of(int u, const GemmParams& p) {
+  Unit r;
+  r.split = u % p.splits;
+  const int tile = u / p.splits;
+  r.n_blk = tile % p.n_nblk;
+  r.m_blk = tile / p.n_nblk;
+  return r;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+                   GemmParams p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  float* s_epi = reinterpret_cast<float*>(smem + C::kStages * C::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_epi + 32 * kBM);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tw);
+    tma_prefetch(&tx);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiThreads);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int units = p.n_mblk * p.n_nblk * p.splits;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      const uint64_t w_policy = policy_evict_first();  // weights stream once
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of(u, p);
+        const int kb0 = w.split * p.kb_per_split;
+        const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStage;
+          mbar_expect_tx(&full[stage], C::kStage);
+          tma_load_2d_hint(&tw, &full[stage], sa, kb * kBK, w.m_blk * kBM, w_policy);
+          tma_load_2d(&tx, &full[stage], sa + kABytes, kb * kBK, w.n_blk * BN);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
+      const Unit w = unit_of(u, p);
+      const int kb0 = w.split * p.kb_per_split;
+      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_addr = smem_u32(smem + stage * C::kStage);
+          const uint32_t b_addr = a_addr + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            umma_bf16(d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                      idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int et = threadIdx.x - 64;
+    const int lane = lane_id();
+    int local = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
+      const Unit w = unit_of(u, p);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int f0 = w.m_blk * kBM;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int tok0 = w.n_blk * BN + c0;
+        if (tok0 >= p.tokens) break;
+        uint32_t r[32];
+        tmem_ld32(tmem + acc * BN + c0 + (static_cast<uint32_t>(q * 32) << 16), r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) s_epi[j * kBM + q * 32 + lane] = __uint_as_float(r[j]);
+        named_bar_sync(1, kEpiThreads);
+        if (p.mode == kEpiSwiGLU) {
+          // rows 0-63 of the tile are gate features, 64-127 the matching up features
+          const int g = et & 7;
+#pragma unroll
+          for (int pass = 0; pass < 2; ++pass) {
+            const int j = pass * 16 + (et >> 3);
+            const int t = tok0 + j;
+            if (t < p.tokens) {
+              __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float gt = s_epi[j * kBM + g * 8 + i];
+                const float up = s_epi[j * kBM + 64 + g * 8 + i];
+                o[i] = __float2bfloat16(silu(gt) * up);
+              }
+              __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) +
+                                   static_cast<size_t>(t) * p.ldo + w.m_blk * 64 + g * 8;
+              *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(o);
+            }
+          }
+        } else if (p.mode == kEpiPartial) {
+          const int g = et & 31;
+#pragma unroll
+          for (int pass = 0; pass < 8; ++pass) {
+            const int j = pass * 4 + (et >> 5);
+            const int t = tok0 + j;
+            if (t < p.tokens) {
+              const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
+              float* dst = p.ws + (static_cast<size_t>(w.split) * p.tokens + t) * p.rows + f0 + g * 4;
+              *reinterpret_cast<float4*>(dst) = v;
+            }
+          }
+        } else if (p.mode == kEpiF32) {
+          const int g = et & 31;
+#pragma unroll
+          for (int pass = 0; pass < 8; ++pass) {
+            const int j = pass * 4 + (et >> 5);
+            const int t = tok0 + j;
+            if (t < p.tokens) {
+              const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
+              float* dst = static_cast<float*>(p.out) + static_cast<size_t>(t) * p.ldo + f0 + g * 4;
+              *reinterpret_cast<float4*>(dst) = v;
+            }
+          }
+        } else {
+          const int g = et & 15;
+#pragma unroll
+          for (int pass = 0; pass < 4; ++pass) {
+            const int j = pass * 8 + (et >> 4);
+            const int t = tok0 + j;
+            if (t < p.tokens) {
+              float v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = s_epi[j * kBM + g * 8 + i];
+              const int f = f0 + g * 8;
+              if (p.mode == kEpiBias || p.mode == kEpiBiasResidual) {
+                const uint4 b = *reinterpret_cast<const uint4*>(p.bias + f);
+                const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&b);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += bf2f(bb[i]);
+              }
+              if (p.mode == kEpiResidual || p.mode == kEpiBiasResidual) {
+                const uint4 rr = *reinterpret_cast<const uint4*>(
+                    p.residual + static_cast<size_t>(t) * p.ldr + f);
+                const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rr);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += bf2f(rb[i]);
+              }
+              __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(v[i]);
+              __nv_bfloat16* dst =
+                  static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo + f;
+              *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(o);
+            }
+          }
+        }
+        named_bar_sync(1, kEpiThreads);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem);
+  }
+}
+
+// Folds K-split partials [split][token][rows] with the requested epilogue.
+__global__ void splitk_reduce_kernel(GemmParams p, int final_mode) {
+  const int out_cols = final_mode == kEpiSwiGLU ? p.rows / 2 : p.rows;
+  const int groups = out_cols / 8;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= p.tokens * groups) return;
+  const int t = idx / groups;
+  const int g = idx % groups;
+  float v[8], u[8];
+  const size_t plane = static_cast<size_t>(p.tokens) * p.rows;
+  if (final_mode == kEpiSwiGLU) {
+    // output features [64*b + i] come from tile rows i (gate) and 64+i (up)
+    const int fo = g * 8;
+    const int blk = fo / 64, off = fo % 64;
+    const int fg = blk * kBM + off, fu = fg + 64;
+    for (int i = 0; i < 8; ++i) v[i] = u[i] = 0.f;
+    for (int s = 0; s < p.splits; ++s) {
+      const float* src = p.ws + s * plane + static_cast<size_t>(t) * p.rows;
+      for (int i = 0; i < 8; ++i) {
+        v[i] += src[fg + i];
+        u[i] += src[fu + i];
+      }
+    }
+    __align__(16) __nv_bfloat16 o[8];
+    for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(silu(v[i]) * u[i]);
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo +
+                              fo) = *reinterpret_cast<uint4*>(o);
+    return;
+  }
+  const int f = g * 8;
+  for (int i = 0; i < 8; ++i) v[i] = 0.f;
+  for (int s = 0; s < p.splits; ++s) {
+    const float4* src =
+        reinterpret_cast<const float4*>(p.ws + s * plane + static_cast<size_t>(t) * p.rows + f);
+    const float4 a = src[0], b = src[1];
+    v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
+    v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+  }
+  if (final_mode == kEpiF32) {
+    float* dst = static_cast<float*>(p.out) + static_cast<size_t>(t) * p.ldo + f;
+    for (int i = 0; i < 8; ++i) dst[i] = v[i];
+    return;
+  }
+  if (final_mode == kEpiBias || final_mode == kEpiBiasResidual)
+    for (int i = 0; i < 8; ++i) v[i] += bf2f(p.bias[f + i]);
+  if (final_mode == kEpiResidual || final_mode == kEpiBiasResidual)
+    for (int i = 0; i < 8; ++i) v[i] += bf2f(p.residual[static_cast<size_t>(t) * p.ldr + f + i]);
+  __align__(16) __nv_bfloat16 o[8];
+  for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(v[i]);
+  *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo + f) =
+      *reinterpret_cast<uint4*>(o);
+}
+
+template <int BN>
+cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, int grid,
+                      cudaStream_t s) {
+  using C = Cfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  gemm_tc_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(tw, tx, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int gemm_pick_bn(int tokens) {
+  return tokens <= 32 ? 32 : tokens <= 64 ? 64 : tokens <= 128 ? 128 : 256;
+}
+
+cudaError_t gemm(const CUtensorMap& w_map, const CUtensorMap& x_map_for_bn, int bn, int rows,
+                 int tokens, int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
+                 const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
+                 cudaStream_t stream, int force_splits) {
+  if (tokens <= 0) return cudaSuccess;
+  if (rows % kBM || K % kBK) return cudaErrorInvalidValue;
+  GemmParams p{};
+  p.rows = rows;
+  p.tokens = tokens;
+  p.K = K;
+  p.n_mblk = rows / kBM;
+  p.n_nblk = (tokens + bn - 1) / bn;
+  p.num_kb = K / kBK;
+  p.mode = mode;
+  p.out = out;
+  p.ldo = ldo;
+  p.bias = bias;
+  p.residual = residual;
+  p.ldr = ldr;
+  p.ws = ws;
+  // K splits: fill the partition when there are fewer tiles than SMs,
+  // keeping >= 4 K blocks per split and the partials inside the workspace.
+  const int tiles = p.n_mblk * p.n_nblk;
+  int splits = 1;
+  if (force_splits > 0) {
+    splits = force_splits;
+  } else if (tiles < sm_count && ws != nullptr) {
+    splits = std::min((sm_count + tiles - 1) / tiles, std::max(1, p.num_kb / 4));
+    splits = std::min(splits, 16);
+  }
+  while (splits > 1 && static_cast<size_t>(splits) * tokens * rows * 4 > ws_bytes) --splits;
+  p.kb_per_split = (p.num_kb + splits - 1) / splits;
+  p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+  const int final_mode = mode;
+  if (p.splits > 1) p.mode = kEpiPartial;
+  const int units = tiles * p.splits;
+  const int grid = std::max(1, std::min(units, sm_count));
+  cudaError_t e;
+  switch (bn) {
+    case 32: e = launch_bn<32>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 64: e = launch_bn<64>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 128: e = launch_bn<128>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 256: e = launch_bn<256>(w_map, x_map_for_bn, p, grid, stream); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess || p.splits == 1) return e;
+  const int out_cols = final_mode == kEpiSwiGLU ? rows / 2 : rows;
+  const int work = tokens * (out_cols / 8);
+  splitk_reduce_kernel<<<(work + 255) / 256, 256, 0, stream>>>(p, final_mode);
+  return cudaGetLastError();
+}
+
+}  // namespace nxd

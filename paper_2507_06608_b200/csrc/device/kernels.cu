@@ -1,0 +1,229 @@
+// Bandwidth-bound helpers of the forward pass: embedding gather, RMSNorm,
+// RoPE + paged KV write, row argmax (greedy sampling), weight init, and the
+// TMA descriptor encoder. All loads/stores are 16-byte vectors.
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+
+#include "device.cuh"
+
+namespace nxd {
+namespace {
+
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
+                             int hidden, __nv_bfloat16* __restrict__ out) {
+  const int t = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<size_t>(tok[t]) * hidden);
+  uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(t) * hidden);
+  for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+// One CTA (256 threads) per row; fp32 sum of squares, bf16 in/out.
+__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows,
+                               int hidden, const __nv_bfloat16* __restrict__ w, float eps,
+                               __nv_bfloat16* __restrict__ out) {
+  const int r = blockIdx.x;
+  const int src_row = rows ? rows[r] : r;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(src_row) * hidden);
+  const int nvec = hidden / 8;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    const uint4 v = xr[i];
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float f = __bfloat162float(b[k]);
+      ss += f * f;
+    }
+  }
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / hidden + eps);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(r) * hidden);
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    const uint4 v = xr[i], ww = wr[i];
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+    const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(&ww);
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      o[k] = __float2bfloat16(__bfloat162float(b[k]) * inv * __bfloat162float(wb[k]));
+    dst[i] = *reinterpret_cast<uint4*>(o);
+  }
+}
+
+// grid = tokens; block = (H + Hkv) * hd/2 / 8 threads... simple: loop.
+// q/k heads rotate pairs (i, i + hd/2) by angle pos * inv_freq[i].
+__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
+                               const int32_t* __restrict__ slot, const float* __restrict__ inv_freq,
+                               int n_heads, int n_kv_heads, int hd, int page_tokens,
+                               __nv_bfloat16* __restrict__ kplane, __nv_bfloat16* __restrict__ vplane) {
+  const int t = blockIdx.x;
+  const int stride = (n_heads + 2 * n_kv_heads) * hd;
+  __nv_bfloat16* row = qkv + static_cast<size_t>(t) * stride;
+  const float p = static_cast<float>(pos[t]);
+  const int half = hd / 2;
+  const int s = slot[t];
+  const int page = s / page_tokens, off = s % page_tokens;
+  // rotation of q and k heads: (n_heads + n_kv_heads) * half pairs
+  const int pairs = (n_heads + n_kv_heads) * half;
+  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+    const int head = i / half, j = i % half;
+    float sn, cs;
+    sincosf(p * inv_freq[j], &sn, &cs);
+    __nv_bfloat16* h = row + head * hd;
+    const float a = __bfloat162float(h[j]), b = __bfloat162float(h[j + half]);
+    const __nv_bfloat16 ra = __float2bfloat16(a * cs - b * sn);
+    const __nv_bfloat16 rb = __float2bfloat16(b * cs + a * sn);
+    if (head < n_heads) {
+      h[j] = ra;
+      h[j + half] = rb;
+    } else {
+      const int kh = head - n_heads;
+      __nv_bfloat16* dst =
+          kplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * page_tokens + off) * hd;
+      dst[j] = ra;
+      dst[j + half] = rb;
+      h[j] = ra;
+      h[j + half] = rb;
+    }
+  }
+  // v heads copy (16 B vectors)
+  const int vvec = n_kv_heads * hd / 8;
+  const __nv_bfloat16* vsrc = row + (n_heads + n_kv_heads) * hd;
+  for (int i = threadIdx.x; i < vvec; i += blockDim.x) {
+    const int kh = (i * 8) / hd, d = (i * 8) % hd;
+    __nv_bfloat16* dst =
+        vplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * page_tokens + off) * hd + d;
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(vsrc + i * 8);
+  }
+}
+
+// One CTA per row; (value, index) reduction with lowest index on ties.
+__global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int32_t* __restrict__ out) {
+  const float* row = logits + static_cast<size_t>(blockIdx.x) * vocab;
+  float best = -FLT_MAX;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best || (v == best && i < idx)) {
+      best = v;
+      idx = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffff, best, o);
+    const int oi = __shfl_xor_sync(0xffffffff, idx, o);
+    if (ov > best || (ov == best && oi < idx)) {
+      best = ov;
+      idx = oi;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < idx)) {
+        best = sv[w];
+        idx = si[w];
+      }
+    out[blockIdx.x] = idx;
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__global__ void fill_random_kernel(__nv_bfloat16* p, size_t n, uint64_t seed, float scale,
+                                   float offset) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint64_t h = mix64(seed ^ mix64(i));
+    const float u = static_cast<float>(h >> 40) * (1.0f / 16777216.0f);  // [0, 1)
+    p[i] = __float2bfloat16(offset + scale * (2.f * u - 1.f));
+  }
+}
+
+}  // namespace
+
+cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int hidden,
+                  __nv_bfloat16* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  embed_kernel<<<n, 128, 0, s>>>(tokens, table, hidden, out);
+  return cudaGetLastError();
+}
+
+cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows, int n, int hidden,
+                    const __nv_bfloat16* w, float eps, __nv_bfloat16* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  rmsnorm_kernel<<<n, 256, 0, s>>>(x, rows, hidden, w, eps, out);
+  return cudaGetLastError();
+}
+
+cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* pos,
+                          const int32_t* slot, const float* inv_freq, int n_heads, int n_kv_heads,
+                          int head_dim, int page_tokens, __nv_bfloat16* kplane,
+                          __nv_bfloat16* vplane, cudaStream_t s) {
+  if (n_tokens == 0) return cudaSuccess;
+  rope_kv_kernel<<<n_tokens, 256, 0, s>>>(qkv, pos, slot, inv_freq, n_heads, n_kv_heads, head_dim,
+                                          page_tokens, kplane, vplane);
+  return cudaGetLastError();
+}
+
+cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  argmax_kernel<<<n, 1024, 0, s>>>(logits, vocab, out);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_random(__nv_bfloat16* p, size_t n, uint64_t seed, float scale, float offset,
+                        cudaStream_t s) {
+  fill_random_kernel<<<1184, 256, 0, s>>>(p, n, seed, scale, offset);
+  return cudaGetLastError();
+}
+
+bool encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t row_stride_bytes, uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {row_stride_bytes};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+}  // namespace nxd

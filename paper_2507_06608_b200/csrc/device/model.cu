@@ -1,0 +1,478 @@
+// The device executor: model weights, paged KV cache, per-lane workspaces,
+// green-context SM layouts, and the forward pass of one scheduled batch.
+//
+// One lane's batch = one launch sequence on the lane's stream:
+//   H2D(metadata) -> embed -> L x [rmsnorm, QKV gemm, rope+KV write,
+//   paged attention, O gemm(+residual), rmsnorm, gate/up gemm(SwiGLU),
+//   down gemm(+residual)] -> rmsnorm(sampled rows) -> lm_head gemm (fp32)
+//   -> argmax -> D2H(tokens)
+// bracketed by CUDA events; the host engine polls the end event.
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "model.cuh"
+
+namespace nxd {
+
+namespace {
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Green-context layouts.
+// ---------------------------------------------------------------------------
+void Partitions::init(int device, bool enable) {
+  cudaDeviceProp prop{};
+  ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  total_sm = prop.multiProcessorCount;
+  ck(cudaStreamCreateWithFlags(&full_stream, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&plain_stream[0], cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&plain_stream[1], cudaStreamNonBlocking), "stream");
+  if (!enable) return;
+  auto sym = [](const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+      throw std::runtime_error(std::string("driver entry point missing: ") + name);
+    return p;
+  };
+  auto get_res = reinterpret_cast<PFN_cuDeviceGetDevResource>(sym("cuDeviceGetDevResource"));
+  auto split = reinterpret_cast<PFN_cuDevSmResourceSplitByCount>(sym("cuDevSmResourceSplitByCount"));
+  auto gen = reinterpret_cast<PFN_cuDevResourceGenerateDesc>(sym("cuDevResourceGenerateDesc"));
+  auto create = reinterpret_cast<PFN_cuGreenCtxCreate>(sym("cuGreenCtxCreate"));
+  auto mkstream = reinterpret_cast<PFN_cuGreenCtxStreamCreate>(sym("cuGreenCtxStreamCreate"));
+  auto get_dev = reinterpret_cast<PFN_cuDeviceGet>(sym("cuDeviceGet"));
+  CUdevice dev;
+  if (get_dev(&dev, device) != CUDA_SUCCESS) throw std::runtime_error("cuDeviceGet");
+  CUdevResource all;
+  if (get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+    throw std::runtime_error("cuDeviceGetDevResource");
+  // Decode lane takes a group of 8k SMs (the green-context granularity on
+  // sm_90+), the prefill lane the remaining SMs of the same split.
+  for (int k = 1; 8 * k + 8 <= static_cast<int>(all.sm.smCount) && k <= 31; ++k) {
+    CUdevResource grp, rest;
+    unsigned n = 1;
+    if (split(&grp, &n, &all, &rest, 0, 8 * k) != CUDA_SUCCESS || n != 1) break;
+    CUdevResourceDesc dg, dr;
+    CUgreenCtx gg, gr;
+    CUstream sg, sr;
+    if (gen(&dg, &grp, 1) != CUDA_SUCCESS || gen(&dr, &rest, 1) != CUDA_SUCCESS ||
+        create(&gg, dg, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        create(&gr, dr, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        mkstream(&sg, gg, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+        mkstream(&sr, gr, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+      throw std::runtime_error("green context creation failed");
+    Layout l;
+    l.decode_sms = static_cast<int>(grp.sm.smCount);
+    l.prefill_sms = static_cast<int>(rest.sm.smCount);
+    l.decode_stream = reinterpret_cast<cudaStream_t>(sg);
+    l.prefill_stream = reinterpret_cast<cudaStream_t>(sr);
+    layouts.push_back(l);
+  }
+  enabled = !layouts.empty();
+}
+
+// Percent -> partition: the integer share maps to an SM target share/100 *
+// total_sm and the layout whose lane size is nearest wins (ties: fewer SMs).
+Partitions::Pick Partitions::pick(int lane_kind, int sm_pct) const {
+  Pick p;
+  if (lane_kind == 3 /*mixed*/ || !enabled) {
+    p.stream = lane_kind == 3 ? full_stream : plain_stream[lane_kind == 2 ? 1 : 0];
+    p.sm_count = total_sm;
+    p.layout = -1;
+    return p;
+  }
+  const double target = sm_pct / 100.0 * total_sm;
+  int best = 0;
+  double best_err = 1e30;
+  for (size_t i = 0; i < layouts.size(); ++i) {
+    const int sms = lane_kind == 2 ? layouts[i].decode_sms : layouts[i].prefill_sms;
+    const double err = std::fabs(sms - target);
+    if (err < best_err - 1e-9) {
+      best_err = err;
+      best = static_cast<int>(i);
+    }
+  }
+  const Layout& l = layouts[best];
+  p.stream = lane_kind == 2 ? l.decode_stream : l.prefill_stream;
+  p.sm_count = lane_kind == 2 ? l.decode_sms : l.prefill_sms;
+  p.layout = best;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// Model.
+// ---------------------------------------------------------------------------
+Model::Model(const nx_device_config& cfg) : cfg_(cfg), a_(cfg.arch) {
+  if (a_.head_dim != 128) throw std::invalid_argument("head_dim must be 128");
+  if (a_.hidden % 128 || a_.ffn % 64 || a_.vocab % 128 || (2 * a_.ffn) % 128)
+    throw std::invalid_argument("hidden/vocab must be multiples of 128, ffn of 64");
+  if (a_.n_heads % a_.n_kv_heads || a_.n_heads / a_.n_kv_heads > 8)
+    throw std::invalid_argument("GQA group must divide heads and be <= 8");
+  if (cfg.page_tokens < 1 || cfg.num_pages < 1) throw std::invalid_argument("bad page geometry");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg.device)
+    throw NoDevice("no CUDA device");
+  ck(cudaSetDevice(cfg.device), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  ck(cudaGetDeviceProperties(&prop, cfg.device), "props");
+  if (prop.major != 10) throw NoDevice("sm_100 device required");
+  parts_.init(cfg.device, cfg.green_contexts != 0);
+  qkv_rows_ = (a_.n_heads + 2 * a_.n_kv_heads) * a_.head_dim;
+  attn_cols_ = a_.n_heads * a_.head_dim;
+  alloc_weights();
+  alloc_kv();
+  lanes_[0].init(this, cfg.max_prefill_tokens);
+  lanes_[1].init(this, cfg.max_decode_batch);
+  // RoPE inverse frequencies theta^(-2i/hd), computed in double, stored fp32.
+  std::vector<float> inv(a_.head_dim / 2);
+  for (int i = 0; i < a_.head_dim / 2; ++i)
+    inv[i] = static_cast<float>(std::pow(static_cast<double>(a_.rope_theta),
+                                         -2.0 * i / static_cast<double>(a_.head_dim)));
+  ck(cudaMalloc(&inv_freq_, inv.size() * sizeof(float)), "malloc inv_freq");
+  ck(cudaMemcpy(inv_freq_, inv.data(), inv.size() * sizeof(float), cudaMemcpyHostToDevice),
+     "copy inv_freq");
+  ck(cudaDeviceSynchronize(), "init sync");
+}
+
+Model::~Model() {
+  cudaDeviceSynchronize();
+  for (void* p : allocs_) cudaFree(p);
+  for (auto& l : lanes_) l.release();
+}
+
+__nv_bfloat16* Model::dalloc_bf16(size_t n) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, n * 2), "cudaMalloc");
+  allocs_.push_back(p);
+  return static_cast<__nv_bfloat16*>(p);
+}
+
+void Model::alloc_weights() {
+  const size_t d = a_.hidden, L = a_.n_layers;
+  uint64_t seed = cfg_.weight_seed;
+  auto next_seed = [&]() { return seed = seed * 6364136223846793005ULL + 1442695040888963407ULL; };
+  const float g = cfg_.weight_gain > 0 ? cfg_.weight_gain : 1.0f;
+  auto uni = [&](size_t k) { return g * std::sqrt(3.0f / static_cast<float>(k)); };
+  auto make = [&](size_t n, float scale, float offset) {
+    __nv_bfloat16* p = dalloc_bf16(n);
+    ck(fill_random(p, n, next_seed(), scale, offset, nullptr), "init weights");
+    weight_bytes_ += n * 2;
+    return p;
+  };
+  emb_ = make(static_cast<size_t>(a_.vocab) * d, 1.0f, 0.f);
+  layers_.resize(L);
+  for (size_t l = 0; l < L; ++l) {
+    LayerW& w = layers_[l];
+    w.attn_norm = make(d, 0.1f, 1.0f);
+    w.qkv = make(static_cast<size_t>(qkv_rows_) * d, uni(d), 0.f);
+    w.qkv_bias = a_.qkv_bias ? make(qkv_rows_, 0.1f, 0.f) : nullptr;
+    w.o = make(d * attn_cols_, uni(attn_cols_), 0.f);
+    w.ffn_norm = make(d, 0.1f, 1.0f);
+    w.gate_up = make(2 * static_cast<size_t>(a_.ffn) * d, uni(d), 0.f);
+    w.down = make(d * a_.ffn, uni(a_.ffn) * 2.0f, 0.f);
+    if (!encode_kmajor(&w.m_qkv, w.qkv, qkv_rows_, d, d * 2, 128) ||
+        !encode_kmajor(&w.m_o, w.o, d, attn_cols_, attn_cols_ * 2, 128) ||
+        !encode_kmajor(&w.m_gate_up, w.gate_up, 2 * a_.ffn, d, d * 2, 128) ||
+        !encode_kmajor(&w.m_down, w.down, d, a_.ffn, static_cast<size_t>(a_.ffn) * 2, 128))
+      throw std::runtime_error("cuTensorMapEncodeTiled failed (weights)");
+  }
+  final_norm_ = make(d, 0.1f, 1.0f);
+  const float lm_gain = cfg_.lm_head_gain > 0 ? cfg_.lm_head_gain : 1.0f;
+  lm_head_ = make(static_cast<size_t>(a_.vocab) * d, lm_gain * std::sqrt(3.0f / d), 0.f);
+  if (!encode_kmajor(&m_lm_, lm_head_, a_.vocab, d, d * 2, 128))
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (lm_head)");
+}
+
+void Model::alloc_kv() {
+  plane_elems_ = static_cast<size_t>(cfg_.num_pages) * a_.n_kv_heads * cfg_.page_tokens *
+                 a_.head_dim;
+  const size_t total = plane_elems_ * 2 * a_.n_layers;
+  kv_ = dalloc_bf16(total);
+  ck(cudaMemset(kv_, 0, total * 2), "kv memset");  // stale pages stay finite
+  kv_bytes_ = total * 2;
+}
+
+// ---------------------------------------------------------------------------
+// Per-lane workspace.
+// ---------------------------------------------------------------------------
+void LaneWs::init(Model* m, int max_tokens) {
+  const nx_arch& a = m->a_;
+  t_max = std::max(max_tokens, 1);
+  const size_t T = t_max;
+  auto alloc = [&](size_t bytes) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, align_up(bytes, 256)), "lane alloc");
+    owned.push_back(p);
+    return p;
+  };
+  x = static_cast<__nv_bfloat16*>(alloc(T * a.hidden * 2));
+  h = static_cast<__nv_bfloat16*>(alloc(T * a.hidden * 2));
+  qkv = static_cast<__nv_bfloat16*>(alloc(T * m->qkv_rows_ * 2));
+  attn = static_cast<__nv_bfloat16*>(alloc(T * m->attn_cols_ * 2));
+  act = static_cast<__nv_bfloat16*>(alloc(T * a.ffn * 2));
+  sample_cap = std::min<int>(t_max, 256);
+  hs = static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(sample_cap) * a.hidden * 2));
+  logits = static_cast<float*>(alloc(static_cast<size_t>(sample_cap) * a.vocab * 4));
+  ws_bytes = 96u << 20;
+  ws = static_cast<float*>(alloc(ws_bytes));
+  part_cap = static_cast<size_t>(8) << 20;  // floats
+  part_o = static_cast<float*>(alloc(part_cap * 4));
+  part_ml = static_cast<float*>(alloc(part_cap / a.head_dim * 2 * 4 + 1024));
+  // metadata (device + pinned mirror)
+  meta_bytes = align_up(T * 12 + T * 16 + T * 8 + (static_cast<size_t>(T) + 1) * 4 * 64 +
+                            static_cast<size_t>(m->cfg_.num_pages) * 4 + 4096,
+                        4096);
+  meta_dev = static_cast<uint8_t*>(alloc(meta_bytes));
+  ck(cudaMallocHost(&meta_host, meta_bytes), "pinned meta");
+  ck(cudaMallocHost(&out_host, static_cast<size_t>(T) * 4), "pinned out");
+  ck(cudaEventCreate(&ev_start), "event");
+  ck(cudaEventCreate(&ev_end), "event");
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t bn = 32u << i;
+    if (!encode_kmajor(&map_h[i], h, T, a.hidden, static_cast<size_t>(a.hidden) * 2, bn) ||
+        !encode_kmajor(&map_attn[i], attn, T, m->attn_cols_, static_cast<size_t>(m->attn_cols_) * 2,
+                       bn) ||
+        !encode_kmajor(&map_act[i], act, T, a.ffn, static_cast<size_t>(a.ffn) * 2, bn) ||
+        !encode_kmajor(&map_hs[i], hs, sample_cap, a.hidden, static_cast<size_t>(a.hidden) * 2, bn))
+      throw std::runtime_error("cuTensorMapEncodeTiled failed (activations)");
+  }
+}
+
+void LaneWs::release() {
+  for (void* p : owned) cudaFree(p);
+  owned.clear();
+  if (meta_host) cudaFreeHost(meta_host);
+  if (out_host) cudaFreeHost(out_host);
+  meta_host = nullptr;
+  out_host = nullptr;
+}
+
+static int bn_index(int bn) { return bn == 32 ? 0 : bn == 64 ? 1 : bn == 128 ? 2 : 3; }
+
+// ---------------------------------------------------------------------------
+// Forward.
+// ---------------------------------------------------------------------------
+void Model::launch(int slot, const nxb::ExecBatch& b) {
+  LaneWs& ws = lanes_[slot];
+  const Partitions::Pick pk = parts_.pick(b.lane_kind, b.sm_pct);
+  ws.stream = pk.stream;
+  ws.sm_count = pk.sm_count;
+  ws.layout = pk.layout;
+  // ---- pack metadata into the pinned mirror ----
+  int T = 0, n_sample = 0, n_pages_total = 0;
+  for (const auto& m : b.members) {
+    T += m.n_tokens;
+    n_sample += m.sample ? 1 : 0;
+    n_pages_total += m.n_pages;
+  }
+  if (T > ws.t_max) throw std::runtime_error("batch exceeds lane token capacity");
+  const int n_seq = static_cast<int>(b.members.size());
+  uint8_t* hp = ws.meta_host;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 16);
+    if (off > ws.meta_bytes) throw std::runtime_error("metadata overflow");
+    return o;
+  };
+  const size_t o_tok = carve(T * 4), o_pos = carve(T * 4), o_slot = carve(T * 4);
+  const size_t o_seq = carve(n_seq * sizeof(AttnSeq));
+  const size_t o_pages = carve(n_pages_total * 4 + 4);
+  const size_t o_rows = carve(n_sample * 4 + 4);
+  int max_work = 0;
+  for (const auto& m : b.members)
+    max_work += (m.n_tokens * (a_.n_heads / a_.n_kv_heads) + 63) / 64;
+  const size_t o_work = carve(static_cast<size_t>(max_work) * sizeof(int2) + 8);
+  int32_t* tok = reinterpret_cast<int32_t*>(hp + o_tok);
+  int32_t* pos = reinterpret_cast<int32_t*>(hp + o_pos);
+  int32_t* slt = reinterpret_cast<int32_t*>(hp + o_slot);
+  AttnSeq* seqs = reinterpret_cast<AttnSeq*>(hp + o_seq);
+  int32_t* pages = reinterpret_cast<int32_t*>(hp + o_pages);
+  int32_t* rows = reinterpret_cast<int32_t*>(hp + o_rows);
+  int2* work = reinterpret_cast<int2*>(hp + o_work);
+  const int group = a_.n_heads / a_.n_kv_heads;
+  int t = 0, pg = 0, ns = 0, nw = 0;
+  ws.dec_seq_count = 0;
+  ws.max_dec_kv = 0;
+  // decode members (q_len == 1) first in the seq table so the decode kernel
+  // can take a prefix; the batch lists them first already.
+  for (int i = 0; i < n_seq; ++i) {
+    const auto& m = b.members[i];
+    AttnSeq& s = seqs[i];
+    s.q_start = t;
+    s.q_len = m.n_tokens;
+    s.kv_len = static_cast<int>(m.start_pos) + m.n_tokens;
+    s.page_off = pg;
+    for (int k = 0; k < m.n_pages; ++k) pages[pg + k] = m.pages[k];
+    for (int k = 0; k < m.n_tokens; ++k) {
+      const int p = static_cast<int>(m.start_pos) + k;
+      tok[t + k] = m.tokens[k];
+      pos[t + k] = p;
+      slt[t + k] = m.pages[p / cfg_.page_tokens] * cfg_.page_tokens + p % cfg_.page_tokens;
+    }
+    if (m.sample) rows[ns++] = t + m.n_tokens - 1;
+    if (!m.is_prefill) {
+      if (i != ws.dec_seq_count) throw std::runtime_error("decode members must come first");
+      ws.dec_seq_count++;
+      ws.max_dec_kv = std::max(ws.max_dec_kv, s.kv_len);
+    } else {
+      for (int r = 0; r < m.n_tokens * group; r += 64) work[nw++] = make_int2(i, r);
+    }
+    t += m.n_tokens;
+    pg += m.n_pages;
+  }
+  ws.tokens = T;
+  ws.n_seq = n_seq;
+  ws.n_work = nw;
+  ws.n_sample = ns;
+  cudaStream_t s = ws.stream;
+  ck(cudaEventRecord(ws.ev_start, s), "event record");
+  ck(cudaMemcpyAsync(ws.meta_dev, hp, off, cudaMemcpyHostToDevice, s), "meta h2d");
+  const uint8_t* dp = ws.meta_dev;
+  ws.d_tok = reinterpret_cast<const int32_t*>(dp + o_tok);
+  ws.d_pos = reinterpret_cast<const int32_t*>(dp + o_pos);
+  ws.d_slot = reinterpret_cast<const int32_t*>(dp + o_slot);
+  ws.d_seqs = reinterpret_cast<const AttnSeq*>(dp + o_seq);
+  ws.d_pages = reinterpret_cast<const int32_t*>(dp + o_pages);
+  ws.d_rows = reinterpret_cast<const int32_t*>(dp + o_rows);
+  ws.d_work = reinterpret_cast<const int2*>(dp + o_work);
+  forward(ws);
+  ck(cudaMemcpyAsync(ws.out_host, ws.d_out_tokens, static_cast<size_t>(ns) * 4,
+                     cudaMemcpyDeviceToHost, s),
+     "tokens d2h");
+  ck(cudaEventRecord(ws.ev_end, s), "event record");
+  ws.pending = true;
+}
+
+void Model::forward(LaneWs& ws) {
+  cudaStream_t s = ws.stream;
+  const int T = ws.tokens;
+  const int d = a_.hidden;
+  const int bn = gemm_pick_bn(T);
+  const int bi = bn_index(bn);
+  const int sm = ws.sm_count;
+  AttnGeom g;
+  g.n_heads = a_.n_heads;
+  g.n_kv_heads = a_.n_kv_heads;
+  g.group = a_.n_heads / a_.n_kv_heads;
+  g.head_dim = a_.head_dim;
+  g.page_tokens = cfg_.page_tokens;
+  g.qkv_stride = qkv_rows_;
+  g.out_stride = attn_cols_;
+  g.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(a_.head_dim));
+  ck(embed(ws.d_tok, T, emb_, d, ws.x, s), "embed");
+  for (int l = 0; l < a_.n_layers; ++l) {
+    const LayerW& w = layers_[l];
+    __nv_bfloat16* kplane = kv_ + (2 * static_cast<size_t>(l)) * plane_elems_;
+    __nv_bfloat16* vplane = kplane + plane_elems_;
+    ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
+    ck(gemm(w.m_qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore, ws.qkv,
+            qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+       "qkv gemm");
+    ck(rope_kv_write(ws.qkv, T, ws.d_pos, ws.d_slot, inv_freq_, a_.n_heads, a_.n_kv_heads,
+                     a_.head_dim, cfg_.page_tokens, kplane, vplane, s),
+       "rope");
+    if (ws.dec_seq_count > 0)
+      ck(decode_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.dec_seq_count, ws.max_dec_kv,
+                          ws.d_pages, ws.attn, ws.part_o, ws.part_ml, ws.part_cap, sm, s),
+         "decode attention");
+    if (ws.n_work > 0)
+      ck(prefill_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.d_work, ws.n_work, ws.d_pages,
+                           ws.attn, s),
+         "prefill attention");
+    ck(gemm(w.m_o, ws.map_attn[bi], bn, d, T, attn_cols_, kEpiResidual, ws.x, d, nullptr, ws.x, d,
+            ws.ws, ws.ws_bytes, sm, s),
+       "o gemm");
+    ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
+    ck(gemm(w.m_gate_up, ws.map_h[bi], bn, 2 * a_.ffn, T, d, kEpiSwiGLU, ws.act, a_.ffn, nullptr,
+            nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+       "gate/up gemm");
+    ck(gemm(w.m_down, ws.map_act[bi], bn, d, T, a_.ffn, kEpiResidual, ws.x, d, nullptr, ws.x, d,
+            ws.ws, ws.ws_bytes, sm, s),
+       "down gemm");
+  }
+  // lm_head over the sampled rows, in chunks of the logits buffer.
+  ws.d_out_tokens = ws.logits_tokens_dev();
+  for (int r0 = 0; r0 < ws.n_sample; r0 += ws.sample_cap) {
+    const int n = std::min(ws.sample_cap, ws.n_sample - r0);
+    ck(rmsnorm(ws.x, ws.d_rows + r0, n, d, final_norm_, a_.rms_eps, ws.hs, s), "final norm");
+    const int sbn = gemm_pick_bn(n);
+    ck(gemm(m_lm_, ws.map_hs[bn_index(sbn)], sbn, a_.vocab, n, d, kEpiF32, ws.logits, a_.vocab,
+            nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+       "lm_head gemm");
+    ck(argmax_rows(ws.logits, n, a_.vocab, ws.d_out_tokens + r0, s), "argmax");
+  }
+}
+
+int32_t* LaneWs::logits_tokens_dev() {
+  if (!out_dev) {
+    ck(cudaMalloc(&out_dev, static_cast<size_t>(t_max) * 4), "out tokens");
+    owned.push_back(out_dev);
+  }
+  return static_cast<int32_t*>(out_dev);
+}
+
+bool Model::done(int slot) {
+  LaneWs& ws = lanes_[slot];
+  if (!ws.pending) return true;
+  const cudaError_t e = cudaEventQuery(ws.ev_end);
+  if (e == cudaErrorNotReady) return false;
+  ck(e, "device batch");
+  finish(ws);
+  return true;
+}
+
+void Model::wait(int slot) {
+  LaneWs& ws = lanes_[slot];
+  if (!ws.pending) return;
+  ck(cudaEventSynchronize(ws.ev_end), "device batch");
+  finish(ws);
+}
+
+void Model::finish(LaneWs& ws) {
+  ws.pending = false;
+  ws.sampled.assign(ws.out_host, ws.out_host + ws.n_sample);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ws.ev_start, ws.ev_end);
+  ws.last_ms = ms;
+}
+
+void Model::copy_logits(int slot, float* host, size_t n_floats) {
+  LaneWs& ws = lanes_[slot];
+  const size_t want = std::min<size_t>(n_floats, static_cast<size_t>(std::min(ws.n_sample, ws.sample_cap)) * a_.vocab);
+  ck(cudaMemcpy(host, ws.logits, want * 4, cudaMemcpyDeviceToHost), "logits d2h");
+}
+
+const __nv_bfloat16* Model::weight_ptr(int tensor, int layer, size_t* elems) const {
+  const size_t d = a_.hidden;
+  if (tensor != 0 && tensor != 8 && tensor != 9 && (layer < 0 || layer >= a_.n_layers))
+    return nullptr;
+  switch (tensor) {
+    case 0: *elems = static_cast<size_t>(a_.vocab) * d; return emb_;
+    case 1: *elems = d; return layers_[layer].attn_norm;
+    case 2: *elems = static_cast<size_t>(qkv_rows_) * d; return layers_[layer].qkv;
+    case 3: *elems = a_.qkv_bias ? qkv_rows_ : 0; return layers_[layer].qkv_bias;
+    case 4: *elems = d * attn_cols_; return layers_[layer].o;
+    case 5: *elems = d; return layers_[layer].ffn_norm;
+    case 6: *elems = 2 * static_cast<size_t>(a_.ffn) * d; return layers_[layer].gate_up;
+    case 7: *elems = d * a_.ffn; return layers_[layer].down;
+    case 8: *elems = d; return final_norm_;
+    case 9: *elems = static_cast<size_t>(a_.vocab) * d; return lm_head_;
+    default: return nullptr;
+  }
+}
+
+}  // namespace nxd

@@ -1,0 +1,129 @@
+// Device executor declarations (see model.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <vector>
+
+#include "device.cuh"
+#include "executor.hpp"
+#include "nexus_b200.h"
+
+namespace nxd {
+
+struct NoDevice : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Pre-instantiated green-context SM layouts: layout k gives the decode lane
+// a group of 8(k+1) SMs and the prefill lane the rest of the same split.
+struct Partitions {
+  struct Layout {
+    int decode_sms = 0, prefill_sms = 0;
+    cudaStream_t decode_stream = nullptr, prefill_stream = nullptr;
+  };
+  struct Pick {
+    cudaStream_t stream = nullptr;
+    int sm_count = 0;
+    int layout = -1;
+  };
+  void init(int device, bool enable);
+  Pick pick(int lane_kind, int sm_pct) const;
+  bool enabled = false;
+  int total_sm = 0;
+  std::vector<Layout> layouts;
+  cudaStream_t full_stream = nullptr;          // monolithic lane: whole GPU
+  cudaStream_t plain_stream[2] = {nullptr, nullptr};  // no partitioning
+};
+
+class Model;
+
+struct LaneWs {
+  void init(Model* m, int max_tokens);
+  void release();
+  int32_t* logits_tokens_dev();
+
+  int t_max = 0;
+  __nv_bfloat16 *x = nullptr, *h = nullptr, *qkv = nullptr, *attn = nullptr, *act = nullptr,
+                *hs = nullptr;
+  float* logits = nullptr;
+  int sample_cap = 0;
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  float *part_o = nullptr, *part_ml = nullptr;
+  size_t part_cap = 0;
+  CUtensorMap map_h[4], map_attn[4], map_act[4], map_hs[4];
+  uint8_t* meta_dev = nullptr;
+  uint8_t* meta_host = nullptr;
+  size_t meta_bytes = 0;
+  int32_t* out_host = nullptr;
+  void* out_dev = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+  std::vector<void*> owned;
+  // current batch
+  cudaStream_t stream = nullptr;
+  int sm_count = 0, layout = -1;
+  int tokens = 0, n_seq = 0, n_work = 0, n_sample = 0, dec_seq_count = 0, max_dec_kv = 0;
+  const int32_t *d_tok = nullptr, *d_pos = nullptr, *d_slot = nullptr, *d_pages = nullptr,
+                *d_rows = nullptr;
+  const AttnSeq* d_seqs = nullptr;
+  const int2* d_work = nullptr;
+  int32_t* d_out_tokens = nullptr;
+  bool pending = false;
+  std::vector<int32_t> sampled;
+  float last_ms = 0.f;
+};
+
+struct LayerW {
+  __nv_bfloat16 *attn_norm, *qkv, *qkv_bias, *o, *ffn_norm, *gate_up, *down;
+  CUtensorMap m_qkv, m_o, m_gate_up, m_down;
+};
+
+class Model : public nxb::Executor {
+ public:
+  explicit Model(const nx_device_config& cfg);
+  ~Model() override;
+
+  void launch(int slot, const nxb::ExecBatch& b) override;
+  bool done(int slot) override;
+  void wait(int slot) override;
+  const std::vector<int32_t>& sampled(int slot) override { return lanes_[slot].sampled; }
+  double device_ms(int slot) override { return lanes_[slot].last_ms; }
+  int32_t vocab() const override { return a_.vocab; }
+  int32_t page_tokens() const override { return cfg_.page_tokens; }
+  int32_t num_pages() const override { return cfg_.num_pages; }
+
+  void copy_logits(int slot, float* host, size_t n_floats);
+  const __nv_bfloat16* weight_ptr(int tensor, int layer, size_t* elems) const;
+  const Partitions& partitions() const { return parts_; }
+  uint64_t weight_bytes() const { return weight_bytes_; }
+  uint64_t kv_bytes() const { return kv_bytes_; }
+  int last_layout(int slot) const { return lanes_[slot].layout; }
+  int last_sm_count(int slot) const { return lanes_[slot].sm_count; }
+
+ private:
+  friend struct LaneWs;
+  void alloc_weights();
+  void alloc_kv();
+  void forward(LaneWs& ws);
+  void finish(LaneWs& ws);
+  __nv_bfloat16* dalloc_bf16(size_t n);
+
+  nx_device_config cfg_;
+  nx_arch a_;
+  int qkv_rows_ = 0, attn_cols_ = 0;
+  Partitions parts_;
+  std::vector<void*> allocs_;
+  __nv_bfloat16 *emb_ = nullptr, *final_norm_ = nullptr, *lm_head_ = nullptr, *kv_ = nullptr;
+  CUtensorMap m_lm_;
+  std::vector<LayerW> layers_;
+  float* inv_freq_ = nullptr;
+  size_t plane_elems_ = 0;
+  uint64_t weight_bytes_ = 0, kv_bytes_ = 0;
+  LaneWs lanes_[2];
+};
+
+}  // namespace nxd

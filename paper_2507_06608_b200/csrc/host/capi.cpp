@@ -4,13 +4,21 @@
 #include <cstring>
 #include <string>
 
+#include "capi_internal.hpp"
 #include "core.hpp"
 #include "engine.hpp"
 
 using namespace nxb;
 
+namespace nxb {
+std::string& last_error() {
+  thread_local std::string s;
+  return s;
+}
+}  // namespace nxb
+
 namespace {
-thread_local std::string g_last_error;
+#define g_last_error (::nxb::last_error())
 
 int fail(int code, const char* what) {
   g_last_error = what;
@@ -76,12 +84,6 @@ int put_plan(const Plan& p, nx_batch_member* out, size_t cap, size_t* n_out, int
 
 struct nx_controller {
   Controller c;
-};
-
-struct nx_engine {
-  explicit nx_engine(const nx_sim_config& cfg) : e(cfg) {}
-  Engine e;
-  std::string err;
 };
 
 extern "C" {

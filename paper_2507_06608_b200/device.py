@@ -1,0 +1,158 @@
+"""Device executor bindings: model geometry presets, the nx_device handle,
+raw device buffers and the single-op GEMM entry point (C-ABI, no torch)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._dev_abi import Arch, BatchDesc, DeviceConfig, DeviceInfo
+
+W_EMBED, W_ATTN_NORM, W_QKV, W_QKV_BIAS, W_O, W_FFN_NORM, W_GATE_UP, W_DOWN, W_FINAL_NORM, W_LM_HEAD = range(10)
+
+
+def lib():
+    return _abi.lib()
+
+
+def _check(rc):
+    if rc != 0:
+        msg = (lib().nx_last_error() or b"").decode()
+        if rc == _abi.NX_ENODEV:
+            raise RuntimeError(f"no usable sm_100 device: {msg}")
+        raise RuntimeError(f"nexus_b200 device error {rc}: {msg}")
+
+
+# ---- bf16 helpers (numpy has no bf16) ------------------------------------
+
+def f32_to_bf16(a: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    r = ((u >> 16) & 1) + np.uint32(0x7FFF)
+    return ((u + r) >> 16).astype(np.uint16)
+
+
+def bf16_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.ascontiguousarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+# ---- geometry presets (kernel view; head_dim fixed at 128) ----------------
+
+def arch(hidden, n_layers, n_heads, n_kv_heads, ffn, vocab, qkv_bias=0, rope_theta=500000.0,
+         rms_eps=1e-5) -> Arch:
+    return Arch(hidden, n_layers, n_heads, n_kv_heads, 128, ffn, vocab, qkv_bias, rope_theta, rms_eps)
+
+
+ARCH_PRESETS = {
+    # C1: the reference's derive(256, 1024, 2, 4, 2) has d = 256; the kernels
+    # are specialized to head_dim 128, so the kernel view is 2 heads x 128
+    # (MHA, so KV bytes/token = 2*L*d*2 = 2048, identical to the cost model).
+    "tiny": dict(hidden=256, n_layers=2, n_heads=2, n_kv_heads=2, ffn=1024, vocab=1024, rope_theta=10000.0),
+    "llama3-8b": dict(hidden=4096, n_layers=32, n_heads=32, n_kv_heads=8, ffn=14336, vocab=128256),
+    "qwen2.5-14b": dict(hidden=5120, n_layers=48, n_heads=40, n_kv_heads=8, ffn=13824, vocab=152064,
+                        qkv_bias=1, rope_theta=1000000.0, rms_eps=1e-6),
+    "llama3-70b": dict(hidden=8192, n_layers=80, n_heads=64, n_kv_heads=8, ffn=28672, vocab=128256),
+}
+
+
+def arch_preset(name: str, **over) -> Arch:
+    kw = dict(ARCH_PRESETS[name])
+    kw.update(over)
+    return arch(**kw)
+
+
+class Device:
+    """nx_device: weights + paged KV cache + per-lane workspaces + SM layouts."""
+
+    def __init__(self, a: Arch, *, num_pages=4096, page_tokens=16, max_prefill_tokens=2048 + 64,
+                 max_decode_batch=64, green_contexts=True, seed=1, weight_gain=1.0, lm_head_gain=4.0,
+                 device=0):
+        self.arch = a
+        cfg = DeviceConfig(a, device, page_tokens, num_pages, max_prefill_tokens, max_decode_batch,
+                           1 if green_contexts else 0, seed, weight_gain, lm_head_gain)
+        self.cfg = cfg
+        self.handle = C.c_void_p()
+        _check(lib().nx_device_create(C.byref(cfg), C.byref(self.handle)))
+
+    def info(self) -> DeviceInfo:
+        i = DeviceInfo()
+        _check(lib().nx_device_get_info(self.handle, C.byref(i)))
+        return i
+
+    def weight(self, tensor: int, layer: int = 0) -> np.ndarray:
+        n = C.c_size_t()
+        _check(lib().nx_device_weight(self.handle, tensor, layer, None, 0, C.byref(n)))
+        out = np.empty(n.value // 2, dtype=np.uint16)
+        if n.value:
+            _check(lib().nx_device_weight(self.handle, tensor, layer, out.ctypes.data, n.value, C.byref(n)))
+        return bf16_to_f32(out)
+
+    def forward(self, members, lane=0, sm_pct=100, want_logits=False):
+        """members: list of dict(tokens=[...], start=int, pages=[...], sample=bool)."""
+        n = len(members)
+        nt = (C.c_int32 * n)(*[len(m["tokens"]) for m in members])
+        sp = (C.c_int64 * n)(*[m["start"] for m in members])
+        sa = (C.c_int32 * n)(*[1 if m.get("sample", True) else 0 for m in members])
+        toks = [t for m in members for t in m["tokens"]]
+        tk = (C.c_int32 * max(1, len(toks)))(*toks)
+        npg = (C.c_int32 * n)(*[len(m["pages"]) for m in members])
+        pgs = [p for m in members for p in m["pages"]]
+        pg = (C.c_int32 * max(1, len(pgs)))(*pgs)
+        b = BatchDesc(lane, sm_pct, n, 0, nt, sp, sa, tk, npg, pg)
+        ns = sum(sa)
+        out = (C.c_int32 * max(1, ns))()
+        logits = np.zeros((max(1, ns), self.arch.vocab), dtype=np.float32) if want_logits else None
+        ms = C.c_double()
+        _check(lib().nx_device_forward(self.handle, C.byref(b), out,
+                                       logits.ctypes.data_as(C.POINTER(C.c_float)) if want_logits else None,
+                                       C.byref(ms)))
+        toks_out = list(out[:ns])
+        return (toks_out, logits[:ns] if want_logits else None, ms.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().nx_device_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
+# ---- raw buffers + single-op entry points --------------------------------
+
+class Buf:
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        self.nbytes = nbytes
+        _check(lib().nx_dev_malloc(max(nbytes, 16), C.byref(self.ptr)))
+
+    @classmethod
+    def from_array(cls, a: np.ndarray) -> "Buf":
+        a = np.ascontiguousarray(a)
+        b = cls(a.nbytes)
+        _check(lib().nx_dev_h2d(b.ptr, a.ctypes.data, a.nbytes))
+        return b
+
+    def to_array(self, shape, dtype) -> np.ndarray:
+        out = np.empty(shape, dtype=dtype)
+        _check(lib().nx_dev_d2h(out.ctypes.data, self.ptr, out.nbytes))
+        return out
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().nx_dev_free(self.ptr)
+            self.ptr = None
+
+
+EPI_STORE, EPI_BIAS, EPI_RESIDUAL, EPI_BIAS_RESIDUAL, EPI_SWIGLU, EPI_F32 = 0, 1, 2, 3, 4, 6
+
+
+def gemm(x: Buf, w: Buf, tokens: int, rows: int, K: int, mode: int, out: Buf, ldo: int,
+         bias: Buf | None = None, residual: Buf | None = None, ldr: int = 0, sm_count: int = 0,
+         splits: int = 0, iters: int = 1) -> float:
+    ms = C.c_float()
+    _check(lib().nx_op_gemm(x.ptr, w.ptr, tokens, rows, K, mode, out.ptr, ldo,
+                            bias.ptr if bias else None, residual.ptr if residual else None, ldr,
+                            sm_count, splits, iters, C.byref(ms)))
+    return ms.value

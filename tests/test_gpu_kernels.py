@@ -1,0 +1,92 @@
+"""GPU numerics of the hand-written kernels through the C-ABI.
+
+GEMM (tcgen05/TMEM/TMA): compared with an fp32 numpy product of the same
+bf16 inputs. Tolerance: |dev - ref| <= 1e-2 * |ref| + 1e-2 * rms(ref)
+(fp32 accumulation, bf16 output rounding = 2^-8 relative).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_2507_06608_b200 import device
+    return device
+
+
+def _rand(D, rng, shape, scale=1.0):
+    return D.f32_to_bf16(rng.standard_normal(shape).astype(np.float32) * scale)
+
+
+def _close(dev, ref, rel=1e-2):
+    tol = rel * np.abs(ref) + rel * np.sqrt(np.mean(ref * ref)) + 1e-6
+    bad = np.abs(dev - ref) > tol
+    assert not bad.any(), f"{bad.sum()} / {bad.size} out of tolerance; max err {np.abs(dev - ref).max()}"
+
+
+SHAPES = [(1, 256, 256), (7, 768, 256), (33, 1024, 512), (64, 6144, 4096), (100, 2048, 1024),
+          (300, 1024, 1024), (2048, 4096, 4096), (2100, 768, 256)]
+
+
+@pytest.mark.parametrize("T,N,K", SHAPES)
+def test_gemm_store(D, T, N, K):
+    rng = np.random.default_rng(T * 7 + N)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    ref = D.bf16_to_f32(x) @ D.bf16_to_f32(w).T
+    bx, bw, bo = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf(T * N * 2)
+    D.gemm(bx, bw, T, N, K, D.EPI_STORE, bo, N)
+    _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), ref)
+
+
+@pytest.mark.parametrize("T,N,K,splits,sms", [(64, 1024, 4096, 4, 0), (5, 768, 2048, 3, 0),
+                                              (200, 1024, 1024, 1, 3), (64, 4096, 4096, 0, 16)])
+def test_gemm_splits_and_small_grids(D, T, N, K, splits, sms):
+    rng = np.random.default_rng(5)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    ref = D.bf16_to_f32(x) @ D.bf16_to_f32(w).T
+    bx, bw, bo = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf(T * N * 2)
+    D.gemm(bx, bw, T, N, K, D.EPI_STORE, bo, N, sm_count=sms, splits=splits)
+    _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), ref)
+
+
+@pytest.mark.parametrize("T,splits", [(9, 1), (64, 4), (500, 1)])
+def test_gemm_bias_residual(D, T, splits):
+    N, K = 1024, 1024
+    rng = np.random.default_rng(T)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    b, r = _rand(D, rng, (N,)), _rand(D, rng, (T, N))
+    bx, bw, bb, br = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf.from_array(b), D.Buf.from_array(r)
+    base = D.bf16_to_f32(x) @ D.bf16_to_f32(w).T
+    for mode, ref in [(D.EPI_BIAS, base + D.bf16_to_f32(b)),
+                      (D.EPI_RESIDUAL, base + D.bf16_to_f32(r)),
+                      (D.EPI_BIAS_RESIDUAL, base + D.bf16_to_f32(b) + D.bf16_to_f32(r))]:
+        bo = D.Buf(T * N * 2)
+        D.gemm(bx, bw, T, N, K, mode, bo, N, bias=bb, residual=br, ldr=N, splits=splits)
+        _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), ref)
+
+
+@pytest.mark.parametrize("T,splits", [(3, 1), (64, 4), (700, 1)])
+def test_gemm_swiglu(D, T, splits):
+    F, K = 1024, 512
+    rng = np.random.default_rng(T + 1)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (2 * F, K), 1 / np.sqrt(K))
+    wf = D.bf16_to_f32(w).reshape(F // 64, 2, 64, K)
+    g = D.bf16_to_f32(x) @ wf[:, 0].reshape(F, K).T
+    u = D.bf16_to_f32(x) @ wf[:, 1].reshape(F, K).T
+    ref = g / (1 + np.exp(-g)) * u
+    bx, bw, bo = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf(T * F * 2)
+    D.gemm(bx, bw, T, 2 * F, K, D.EPI_SWIGLU, bo, F, splits=splits)
+    _close(D.bf16_to_f32(bo.to_array((T, F), np.uint16)), ref)
+
+
+def test_gemm_f32_logits(D):
+    T, N, K = 40, 1024 * 8, 512
+    rng = np.random.default_rng(9)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    ref = D.bf16_to_f32(x) @ D.bf16_to_f32(w).T
+    bx, bw, bo = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf(T * N * 4)
+    D.gemm(bx, bw, T, N, K, D.EPI_F32, bo, N)
+    dev = bo.to_array((T, N), np.float32)
+    np.testing.assert_allclose(dev, ref, rtol=1e-3, atol=1e-3 * np.abs(ref).max())
