@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark: SLO goodput of the Nexus executor on Llama-3.1-8B, one B200.
+
+A *step* serves one fixed synthetic trace segment end to end: `--requests`
+ShareGPT-shaped requests (reference presets.cpp:58-66 length fits) with
+Poisson arrivals at `--rate` req/s, submitted through the C-ABI
+(nx_submit_with_tokens: prompt ids from host buffers), executed by the
+device-clock step executor (prefill and decode lanes on green-context SM
+partitions, split chosen per launch by the cost model), with every sampled
+token copied back to the host, then read out through nx_engine_tokens.
+
+value  = SLO goodput on the engine clock: output tokens of requests with
+         TTFT <= --slo-ttft and per-request p99 TBT <= --slo-tbt, divided by
+         the makespan (first arrival -> last finish), summed over timed steps.
+e2e    = the same good tokens divided by the client wall time of the whole
+         call (submit from host buffers + serve + token read-back).
+roofline = the dominant kernel class by device time (sampled CUDA-event
+         pairs on the launching green-context stream), algorithmic bytes or
+         FLOPs per launch / its event time, vs MEASURED_PEAKS.json.
+
+`--impl reference` runs the reference's own CPU implementation of the path
+(oracle/_ref: nexussim compiled from /root/reference) on the same trace and
+config; it cannot execute a model, so its goodput is computed on its
+cost-model clock with the B200 GpuSpec (reported with its CPU wall time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+# Reference ModelConfig preset "8b" (presets.cpp:16) drives the cost model;
+# the kernel view is Llama-3.1-8B (GQA 32/8, SwiGLU 14336, vocab 128256).
+REF_KVBPT_8B = 2 * 32 * 4096 * 2       # reference formula, bytes/token
+REAL_KVBPT_8B = 2 * 32 * 8 * 128 * 2   # real GQA bytes/token
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=4)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="nexus", choices=["nexus", "reference"])
+    p.add_argument("--engine", default="nexus", choices=["nexus", "static", "monolithic"])
+    p.add_argument("--rate", type=float, default=24.0)
+    p.add_argument("--requests", type=int, default=120)
+    p.add_argument("--model", default="llama3-8b")
+    p.add_argument("--kv-gb", type=float, default=80.0)
+    p.add_argument("--slo-ttft", type=float, default=1.0)
+    p.add_argument("--slo-tbt", type=float, default=0.05)
+    p.add_argument("--profile-every", type=int, default=8)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--no-green", action="store_true")
+    p.add_argument("--calib", default=os.path.join(REPO, "profiles", "b200_llama3_8b"),
+                   help="calibration base path (.calib + .json from paper_2507_06608_b200.calibrate); "
+                        "'none' = reference default profile and nominal B200 spec")
+    p.add_argument("--no-bw-ext", action="store_true", help="disable the share-dependent bandwidth term")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---- metrics from a reference-format event log (same code for both arms) --
+
+def log_metrics(event_log: str, slo_ttft: float, slo_tbt: float):
+    arrival, times, finish = {}, {}, {}
+    for line in event_log.splitlines():
+        c = line.split("\t")
+        t, kind, members = float(c[0]), c[2], c[3]
+        if members == "-":
+            continue
+        for m in members.split(","):
+            rid, _tok, emitted = (int(x) for x in m.split(":"))
+            if kind == "arrival":
+                arrival[rid] = t
+            elif kind == "complete" and emitted:
+                times.setdefault(rid, []).extend([t] * emitted)
+            elif kind == "finish":
+                finish[rid] = t
+    ttft, gaps_all, good, out_tokens = [], [], 0, 0
+    for rid, f in finish.items():
+        ts = times[rid]
+        tt = ts[0] - arrival[rid]
+        gaps = [b - a for a, b in zip(ts, ts[1:])]
+        ttft.append(tt)
+        gaps_all.extend(gaps)
+        out_tokens += len(ts)
+        p99 = sorted(gaps)[max(0, -(-99 * len(gaps) // 100) - 1)] if gaps else 0.0
+        if tt <= slo_ttft and p99 <= slo_tbt:
+            good += len(ts)
+    span = (max(finish.values()) - min(arrival.values())) if finish else 0.0
+    return dict(good_tokens=good, out_tokens=out_tokens, makespan=span, ttft=ttft, tbt=gaps_all,
+                completed=len(finish))
+
+
+def nearest_rank(v, p):
+    """Nearest-rank percentile (reference metrics.cpp:30-38)."""
+    if not v:
+        return 0.0
+    v = sorted(v)
+    import math
+    k = min(len(v), max(1, math.ceil(p / 100.0 * len(v))))
+    return v[k - 1]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.rows, self.proc, self.gpu = [], None, gpu_index
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sms = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        loaded = sorted(sms)
+        return {"sm_mhz": loaded[len(loaded) // 2] if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")  # scalar barrier / max only; no data-path collective
+        return rank, world, local, dist
+    return rank, world, local, None
+
+
+def load_calib(base):
+    """(peak_compute, peak_bandwidth, profile, bw_sat) from a calibration, or None."""
+    if not base or base == "none" or not os.path.exists(base + ".json"):
+        return None
+    import paper_2507_06608_b200 as nx
+    d = json.load(open(base + ".json"))
+    prof, _ = nx.parse_kernel_profile(open(base + ".calib").read())
+    return d["gpu_spec"]["peak_compute"], d["gpu_spec"]["peak_bandwidth"], prof, d["bw_sat"]
+
+
+def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True):
+    m = nx.model_preset("8b")
+    slack = 4096
+    cap_tokens = (num_pages - slack) * page_tokens
+    cal = load_calib(calib)
+    C, B, prof, bw_sat = (1.6595e15, 6.5562e12, None, None) if cal is None else cal
+    g = nx.gpu_spec(148, C, B, cap_tokens * REF_KVBPT_8B)
+    kind = {"nexus": nx.NX_ENGINE_NEXUS, "static": nx.NX_ENGINE_STATIC,
+            "monolithic": nx.NX_ENGINE_MONOLITHIC}[engine]
+    return nx.sim_config(m, g, kind=kind, clock_mode=clock_mode, profile=prof,
+                         bw_sat=bw_sat if bw_ext else None)
+
+
+def run_reference(args, rank, world, dist):
+    """The reference's CPU implementation (oracle/_ref), same trace + config."""
+    if rank != 0:
+        return
+    import paper_2507_06608_b200 as nx
+    from oracle import reference
+    if not reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libnexussim_ref.so not built"}))
+        return
+    page_tokens = 16
+    num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * REAL_KVBPT_8B))
+    cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext)
+    good = span = wall = 0.0
+    ttft, tbt, decisions = [], [], 0
+    for step in range(args.warmup + args.steps):
+        trace = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed + step)
+        t0 = time.perf_counter()
+        r = reference.run(cfg, trace)
+        t1 = time.perf_counter()
+        if step < args.warmup:
+            continue
+        m = log_metrics(r["event_log"], args.slo_ttft, args.slo_tbt)
+        good += m["good_tokens"]
+        span += m["makespan"]
+        wall += t1 - t0
+        ttft += m["ttft"]
+        tbt += m["tbt"]
+        decisions += r["decision_log"].count("\n") - 1
+    value = good / span if span else 0.0
+    line = {
+        "impl": "reference", "metric": "goodput_tok_per_s_at_slo", "value": value, "unit": "tok/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "Llama-3.1-8B (reference 8b preset), sharegpt Poisson", "rate_rps": args.rate,
+                   "requests_per_step": args.requests, "engine": args.engine,
+                   "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt}},
+        "ttft_p50": nearest_rank(ttft, 50), "ttft_p99": nearest_rank(ttft, 99),
+        "tbt_p50": nearest_rank(tbt, 50), "tbt_p99": nearest_rank(tbt, 99),
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": 1, "kind": "reference",
+                         "sample": f"{args.steps} x {args.requests} sharegpt requests on nexussim's cost-model "
+                                   f"clock; CPU wall {wall:.3f}s, {1e6 * wall / max(1, decisions):.2f} us/decision"},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    rank, world, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world, dist)
+        return
+    import numpy as np
+    import paper_2507_06608_b200 as nx
+    from paper_2507_06608_b200 import device as D
+
+    page_tokens = 16
+    num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * REAL_KVBPT_8B))
+    dev = D.Device(D.arch_preset(args.model), num_pages=num_pages, page_tokens=page_tokens,
+                   max_prefill_tokens=2048 + 64, max_decode_batch=64, green_contexts=not args.no_green,
+                   seed=args.seed, device=local)
+    dev.set_profiling(args.profile_every)
+    cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext)
+    vocab = dev.arch.vocab
+    rng = np.random.default_rng(args.seed + 7919 * rank)
+
+    def one_step(step):
+        trace = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed + step + 1000 * rank)
+        prompts = [rng.integers(0, vocab, t.prompt_len, dtype=np.int32) for t in trace]
+        t0 = time.perf_counter()
+        eng = nx.Engine(cfg, device=dev)
+        eng.set_slo(args.slo_ttft, args.slo_tbt)
+        eng.set_logging(True, False)
+        for t, p in zip(trace, prompts):
+            eng.submit(t, p.tolist())
+        eng.run()
+        toks = [eng.tokens(t.id) for t in trace]
+        t1 = time.perf_counter()
+        m = log_metrics(eng.event_log(), args.slo_ttft, args.slo_tbt)
+        m["wall"] = t1 - t0
+        m["launches"] = eng.stats().launches
+        m["h2d"] = sum(4 * t.prompt_len for t in trace)
+        m["d2h"] = 4 * sum(len(x) - t.prompt_len for x, t in zip(toks, trace))
+        m["decisions"] = eng.decision_log().count("\n") - 1
+        m["switches"] = eng.stats().switches
+        eng.close()
+        return m
+
+    for s in range(args.warmup):
+        one_step(s)
+    dev.reset_kernel_stats()
+    k0 = dev.kernel_stats().kernel_launches
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    clocks.start()
+    results = [one_step(args.warmup + s) for s in range(args.steps)]
+    clk = clocks.stop()
+    ks = dev.kernel_stats()
+    good = sum(r["good_tokens"] for r in results)
+    span = sum(r["makespan"] for r in results)
+    wall = sum(r["wall"] for r in results)
+    if dist:
+        import torch
+        t = torch.tensor([good, span, wall], dtype=torch.float64)
+        w = torch.tensor([wall], dtype=torch.float64)
+        dist.all_reduce(t)  # sum good tokens / spans over ranks
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        good, span_sum, _ = t.tolist()
+        wall_max = w.item()
+    else:
+        span_sum, wall_max = span, wall
+    value = good / (span_sum / world) if span_sum else 0.0  # whole-job tok/s
+    e2e = good / wall_max if wall_max else 0.0
+    ttft = [x for r in results for x in r["ttft"]]
+    tbt = [x for r in results for x in r["tbt"]]
+    pk, pk_kind = peaks()
+    names = ["gemm_decode", "gemm_prefill", "attn_decode", "attn_prefill", "other"]
+    classes = {}
+    for i, n in enumerate(names):
+        if ks.launches[i]:
+            per_ms = ks.ms[i] / ks.launches[i]
+            classes[n] = {"ms_total_sampled": ks.ms[i], "launches_sampled": ks.launches[i],
+                          "GBps": ks.bytes[i] / ks.ms[i] / 1e6 if ks.ms[i] else 0.0,
+                          "TFLOPs": ks.flops[i] / ks.ms[i] / 1e9 if ks.ms[i] else 0.0,
+                          "avg_launch_ms": per_ms}
+    dom = max(classes, key=lambda n: classes[n]["ms_total_sampled"]) if classes else None
+    roof = None
+    if dom:
+        c = classes[dom]
+        i = names.index(dom)
+        tensor = dom in ("gemm_prefill", "attn_prefill")
+        if tensor:
+            ach, peak, unit = c["TFLOPs"], pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), "TFLOP/s"
+        else:
+            ach, peak, unit = c["GBps"], pk["hbm_gbs"], "GB/s"
+        roof = {"bound": "tensor" if tensor else "hbm", "kernel_class": dom, "achieved": ach, "peak": peak,
+                "peak_source": pk_kind + (" sustained" if tensor else ""), "unit": unit,
+                "frac": ach / peak if peak else None, "traffic": None,
+                "algorithmic_per_launch": (ks.flops[i] if tensor else ks.bytes[i]) / ks.launches[i],
+                "share_of_sampled_device_time": ks.ms[i] / ks.batch_ms_sampled if ks.batch_ms_sampled else None}
+    if rank != 0:
+        return
+    cpu = None
+    try:
+        from oracle import reference
+        if reference.available():
+            tr = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed)
+            vcfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext)
+            t0 = time.perf_counter()
+            rr = reference.run(vcfg, tr)
+            cw = time.perf_counter() - t0
+            mm = log_metrics(rr["event_log"], args.slo_ttft, args.slo_tbt)
+            cpu = {"value": mm["good_tokens"] / mm["makespan"] if mm["makespan"] else 0.0, "unit": "tok/s",
+                   "cores": 1, "kind": "reference",
+                   "sample": f"1 x {args.requests} sharegpt requests through nexussim (cost-model clock, "
+                             f"B200 GpuSpec); CPU wall {cw:.3f}s"}
+    except Exception as e:  # the baseline is reported, never required
+        cpu = {"unavailable": str(e)}
+    line = {
+        "metric": "goodput_tok_per_s_at_slo", "value": value, "unit": "tok/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, sharegpt-shaped lengths, random prompt ids)",
+        "config": {"workload": "Llama-3.1-8B bf16, 1 B200 per rank, sharegpt Poisson (BASELINE configs[1])",
+                   "rate_rps": args.rate, "requests_per_step": args.requests, "engine": args.engine,
+                   "clock": "device", "green_contexts": not args.no_green,
+                   "calibration": os.path.basename(args.calib) if load_calib(args.calib) else "none",
+                   "bw_ext": not args.no_bw_ext,
+                   "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt},
+                   "kv_pool_gb": args.kv_gb, "parallelism": f"replicas x{world}",
+                   "l2": "inputs > L2 (16 GB weights streamed per decode step)"},
+        "ttft_p50": nearest_rank(ttft, 50), "ttft_p99": nearest_rank(ttft, 99),
+        "tbt_p50": nearest_rank(tbt, 50), "tbt_p99": nearest_rank(tbt, 99),
+        "completed": sum(r["completed"] for r in results), "good_tokens": good,
+        "output_tokens": sum(r["out_tokens"] for r in results),
+        "decisions": sum(r["decisions"] for r in results), "switches": sum(r["switches"] for r in results),
+        "e2e": {"value": e2e, "unit": "tok/s", "h2d_bytes_per_step": sum(r["h2d"] for r in results) // args.steps,
+                "d2h_bytes_per_step": sum(r["d2h"] for r in results) // args.steps},
+        "gpu_launches": int(ks.kernel_launches - k0),
+        "roofline": roof, "kernel_classes": classes, "clocks": clk, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

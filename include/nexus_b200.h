@@ -120,13 +120,26 @@ typedef struct nx_engine_config {
   uint64_t max_events;
 } nx_engine_config;
 
-/* SimConfig (simulator.hpp:45-51). */
+/* Cost-model extension (new, off by default => reference-exact): the HBM
+ * bandwidth an operator can draw grows with its SM share until bw_sat,
+ *   mem_s = bytes / (B * min(1, share / bw_sat[kind])),
+ * because on B200 one SM streams only ~1/90 of peak HBM bandwidth. The
+ * reference's memory time ignores the share (costmodel.cpp:33), which makes
+ * its controller starve decode of SMs. */
+typedef struct nx_cost_ext {
+  int32_t enabled;
+  int32_t _pad0;
+  double bw_sat[5]; /* per operator kind, in (0, 1] */
+} nx_cost_ext;
+
+/* SimConfig (simulator.hpp:45-51) + the cost-model extension. */
 typedef struct nx_sim_config {
   nx_model_config model;
   nx_gpu_spec gpu;
   nx_controller_config ctrl;
   nx_kernel_profile profile;
   nx_engine_config engine;
+  nx_cost_ext ext;
 } nx_sim_config;
 
 /* Request (domain.hpp:58-72), trace view. */
@@ -201,6 +214,9 @@ typedef struct nx_breakdown {
 /* compute_latency, Eq. 5 (costmodel.cpp:8-14). Returns NX_EINVAL for share <= 0. */
 int nx_compute_latency(double flops, double share, nx_saturation_curve curve,
                        double peak_compute, double* out_s);
+/* Installs a cost-model extension for the nx_phase_latency_isolated /
+ * nx_decode_latency_contended calls of this thread (NULL = reference model). */
+int nx_set_cost_ext(const nx_cost_ext* ext);
 /* phase_latency_isolated (costmodel.cpp:43-49). */
 int nx_phase_latency_isolated(const nx_op_workload* ops, size_t n_ops, double share,
                               const nx_gpu_spec* gpu, const nx_kernel_profile* prof,
@@ -512,6 +528,33 @@ typedef struct nx_batch_desc {
 } nx_batch_desc;
 int nx_device_forward(nx_device* dev, const nx_batch_desc* b, int32_t* sampled, float* logits,
                       double* device_ms);
+/* Asynchronous halves of nx_device_forward: launch on the lane's partition
+ * stream and return; wait for that lane's batch (co-location experiments). */
+int nx_device_launch(nx_device* dev, const nx_batch_desc* b);
+int nx_device_wait(nx_device* dev, int32_t lane, int32_t* sampled, float* logits,
+                   double* device_ms);
+
+/* Kernel-class timing (CUDA events on the launching stream, every
+ * `sample_every`-th batch per lane; 0 disables) with algorithmic work. */
+#define NX_K_GEMM_DECODE 0  /* projections on the decode lane (HBM-bound weight stream) */
+#define NX_K_GEMM_PREFILL 1 /* projections on the prefill / mixed lane (tensor-bound) */
+#define NX_K_ATTN_DECODE 2  /* split-KV paged decode attention (HBM-bound KV stream) */
+#define NX_K_ATTN_PREFILL 3 /* causal paged prefill attention */
+#define NX_K_OTHER 4        /* norms, RoPE/KV write, embedding, argmax */
+#define NX_K_CLASSES 5
+typedef struct nx_kernel_stats {
+  double ms[NX_K_CLASSES];
+  double bytes[NX_K_CLASSES];  /* algorithmic bytes moved */
+  double flops[NX_K_CLASSES];  /* algorithmic FLOPs */
+  uint64_t launches[NX_K_CLASSES];
+  uint64_t batches_sampled;
+  double batch_ms_sampled; /* whole-batch device time of the sampled batches */
+  uint64_t kernel_launches; /* every kernel this device launched (all batches) */
+  uint64_t batches;         /* every batch this device ran */
+} nx_kernel_stats;
+int nx_device_set_profiling(nx_device* dev, int32_t sample_every);
+int nx_device_kernel_stats(const nx_device* dev, nx_kernel_stats* out);
+int nx_device_reset_kernel_stats(nx_device* dev);
 
 /* ---- raw device plumbing + single-op entry points (tests / profiling) --- */
 int nx_dev_malloc(size_t bytes, void** p);

@@ -96,10 +96,13 @@ def compute_latency(flops, share, c, peak):  # costmodel.cpp:8-14
     return flops / (c.r_sat * peak) * (1.0 + c.lambda_ * (share - c.r_sat))
 
 
-def breakdown(ops, share, gpu, prof, dbw=0.0):  # costmodel.cpp:18-41
+def breakdown(ops, share, gpu, prof, dbw=0.0, ext=None):  # costmodel.cpp:18-41
+    """ext: per-op bw_sat list (the product's flagged nx_cost_ext), or None."""
     total = attn = 0.0
     for kind, fl, mem, kv, is_attn in ops:
         bw = dbw if (kind == ATTN_DECODE and dbw > 0) else gpu.peak_bandwidth
+        if ext is not None and share < ext[kind]:
+            bw = bw * (share / ext[kind])
         comp = compute_latency(fl, share, _curve(prof, kind), gpu.peak_compute)
         ms = mem / bw
         t = ms if comp < ms else comp
@@ -109,7 +112,7 @@ def breakdown(ops, share, gpu, prof, dbw=0.0):  # costmodel.cpp:18-41
     return total, attn
 
 
-def contended(dops, share, pbd, pops, gpu, prof):  # costmodel.cpp:66-96
+def contended(dops, share, pbd, pops, gpu, prof, ext=None):  # costmodel.cpp:66-96
     p = 0.0 if pbd[0] <= 0 else pbd[1] / pbd[0]
     m_p1 = m_p2 = m_d = 0.0
     for kind, fl, mem, kv, is_attn in pops:
@@ -122,7 +125,7 @@ def contended(dops, share, pbd, pops, gpu, prof):  # costmodel.cpp:66-96
             m_d += kv
     B = gpu.peak_bandwidth
     bw = (m_d / (m_d + m_p1) * p * B + m_d / (m_d + m_p2) * (1.0 - p) * B) if m_d > 0 else B
-    return breakdown(dops, share, gpu, prof, bw)
+    return breakdown(dops, share, gpu, prof, bw, ext)
 
 
 # ---- schedulers.cpp --------------------------------------------------------
@@ -228,6 +231,7 @@ def run_port(cfg, trace, replay=None):
     """Runs the engine; returns (event_log, decision_log). `replay` replaces
     the cost-model latency of the k-th launch by replay[k]."""
     m, gpu, ctrl, prof, eng = cfg.model, cfg.gpu, cfg.ctrl, cfg.profile, cfg.engine
+    ext = list(cfg.ext.bw_sat) if cfg.ext.enabled else None
     kind = eng.kind  # 0 nexus, 1 monolithic, 2 static
     dynamic, mono = kind == 0, kind == 1
     ctl = Controller(eng.static_r_p if kind == 2 else 50, ctrl)
@@ -296,8 +300,8 @@ def run_port(cfg, trace, replay=None):
     def decide(launching_prefill, ops):  # controller_decide, :290-324
         pre = P.ops if P.busy else (ops if launching_prefill else provisional_prefill())
         dco = D.ops if D.busy else (provisional_decode() if launching_prefill else ops)
-        pm = (bool(pre), lambda s: breakdown(pre, s / 100.0, gpu, prof)[0])
-        dm = (bool(dco), lambda s: breakdown(dco, s / 100.0, gpu, prof)[0])
+        pm = (bool(pre), lambda s: breakdown(pre, s / 100.0, gpu, prof, 0.0, ext)[0])
+        dm = (bool(dco), lambda s: breakdown(dco, s / 100.0, gpu, prof, 0.0, ext)[0])
         mode, cand, applied, sw, q = ctl.decide(st["used"], gpu.kv_capacity_bytes, pm, dm)
         dec_log.append(f"{_g(st['clock'])}\t{_g(float(st['used']) / float(gpu.kv_capacity_bytes))}\t{mode}\t"
                        f"{cand}\t{applied}\t{int(sw)}\t{q}\n")
@@ -321,7 +325,8 @@ def run_port(cfg, trace, replay=None):
         ops = decode_ops(m, ctxs(ms))
         r_p = decide(False, ops) if dynamic else ctl.r_p
         share = (100 - r_p) / 100.0
-        D.bd = contended(ops, share, P.bd, P.ops, gpu, prof) if P.busy else breakdown(ops, share, gpu, prof)
+        D.bd = (contended(ops, share, P.bd, P.ops, gpu, prof, ext) if P.busy
+                else breakdown(ops, share, gpu, prof, 0.0, ext))
         D.dec, D.pre, D.ops, D.r_p = ms, [], ops, r_p
         begin(D, "decode", D.bd[0])
 
@@ -334,7 +339,7 @@ def run_port(cfg, trace, replay=None):
             return
         ops = prefill_ops(m, chunks(kept))
         r_p = decide(True, ops) if dynamic else ctl.r_p
-        P.bd = breakdown(ops, r_p / 100.0, gpu, prof)
+        P.bd = breakdown(ops, r_p / 100.0, gpu, prof, 0.0, ext)
         P.pre, P.dec, P.ops, P.r_p = kept, [], ops, r_p
         begin(P, "prefill", P.bd[0])
 
@@ -350,7 +355,7 @@ def run_port(cfg, trace, replay=None):
         if not d and not p:
             return
         ops = mixed_ops(m, chunks(p), ctxs(d))
-        P.bd = breakdown(ops, 1.0, gpu, prof)
+        P.bd = breakdown(ops, 1.0, gpu, prof, 0.0, ext)
         P.dec, P.pre, P.ops, P.r_p = d, p, ops, 100
         begin(P, "mixed", P.bd[0])
 

@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 from typing import Callable, Iterable, Sequence
 
 from . import _abi
-from ._abi import (BatchMember, Breakdown, ControllerConfig, DecodeCandidate, EngineConfig,
+from ._abi import (BatchMember, Breakdown, ControllerConfig, CostExt, DecodeCandidate, EngineConfig,
                    GpuSpec, KernelProfile, ModelConfig, OpWorkload, PartitionState, PhaseModel,
                    PrefillEntry, Request, SaturationCurve, SimConfig)
 from ._abi import (NX_CLOCK_DEVICE, NX_CLOCK_REPLAY, NX_CLOCK_VIRTUAL, NX_ENGINE_MONOLITHIC,
@@ -89,7 +89,9 @@ def sim_config(model: ModelConfig, gpu: GpuSpec, *, kind: int = NX_ENGINE_NEXUS,
                static_r_p: int = 50, prefill_policy: int = NX_PREFILL_SPF,
                clock_mode: int = NX_CLOCK_VIRTUAL, ctrl: ControllerConfig | None = None,
                profile: KernelProfile | None = None, timeout_sim_s: float = 3600.0,
-               max_events: int = 10_000_000) -> SimConfig:
+               max_events: int = 10_000_000, bw_sat: Sequence[float] | None = None) -> SimConfig:
+    """SimConfig; bw_sat (5 per-op shares) enables the SM-share-limited HBM
+    bandwidth extension of the cost model (nx_cost_ext), None = reference."""
     cfg = SimConfig()
     cfg.model = model
     cfg.gpu = gpu
@@ -99,7 +101,17 @@ def sim_config(model: ModelConfig, gpu: GpuSpec, *, kind: int = NX_ENGINE_NEXUS,
     e.kind, e.static_r_p, e.prefill_policy, e.clock_mode = kind, static_r_p, prefill_policy, clock_mode
     e.timeout_sim_s, e.max_events = timeout_sim_s, max_events
     cfg.engine = e
+    if bw_sat is not None:
+        cfg.ext = CostExt(1, 0, (C.c_double * 5)(*bw_sat))
     return cfg
+
+
+def set_cost_ext(bw_sat: Sequence[float] | None) -> None:
+    """Extension for the standalone cost-model calls (phase_latency_isolated, ...)."""
+    if bw_sat is None:
+        _check(lib().nx_set_cost_ext(None))
+    else:
+        _check(lib().nx_set_cost_ext(C.byref(CostExt(1, 0, (C.c_double * 5)(*bw_sat)))))
 
 
 def validate_config(model, gpu, ctrl, prof) -> list[str]:

@@ -61,9 +61,13 @@ class EngineConfig(C.Structure):
                 ("max_events", C.c_uint64)]
 
 
+class CostExt(C.Structure):
+    _fields_ = [("enabled", C.c_int32), ("_pad0", C.c_int32), ("bw_sat", C.c_double * 5)]
+
+
 class SimConfig(C.Structure):
     _fields_ = [("model", ModelConfig), ("gpu", GpuSpec), ("ctrl", ControllerConfig),
-                ("profile", KernelProfile), ("engine", EngineConfig)]
+                ("profile", KernelProfile), ("engine", EngineConfig), ("ext", CostExt)]
 
 
 class Request(C.Structure):
@@ -162,6 +166,7 @@ _PROTOS = {
     "nx_decode_latency_contended": (C.c_int, [P(OpWorkload), sz, C.c_double, P(Breakdown),
                                               P(OpWorkload), sz, P(GpuSpec), P(KernelProfile),
                                               P(Breakdown)]),
+    "nx_set_cost_ext": (C.c_int, [C.c_void_p]),
     "nx_min_phase_latency": (C.c_double, [P(OpWorkload), sz, P(GpuSpec), P(KernelProfile)]),
     "nx_select_mode": (C.c_int, [C.c_int64, C.c_int64, C.c_double]),
     "nx_adjust_partition": (C.c_int, [C.c_int32, P(PartitionState), P(PhaseModel),

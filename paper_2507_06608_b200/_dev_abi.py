@@ -33,13 +33,25 @@ class BatchDesc(C.Structure):
                 ("tokens", P(C.c_int32)), ("n_pages", P(C.c_int32)), ("pages", P(C.c_int32))]
 
 
+class KernelStats(C.Structure):
+    _fields_ = [("ms", C.c_double * 5), ("bytes", C.c_double * 5), ("flops", C.c_double * 5),
+                ("launches", C.c_uint64 * 5), ("batches_sampled", C.c_uint64),
+                ("batch_ms_sampled", C.c_double), ("kernel_launches", C.c_uint64),
+                ("batches", C.c_uint64)]
+
+
 PROTOS = {
+    "nx_device_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
+    "nx_device_kernel_stats": (C.c_int, [C.c_void_p, P(KernelStats)]),
+    "nx_device_reset_kernel_stats": (C.c_int, [C.c_void_p]),
     "nx_device_create": (C.c_int, [P(DeviceConfig), P(C.c_void_p)]),
     "nx_device_destroy": (None, [C.c_void_p]),
     "nx_device_get_info": (C.c_int, [C.c_void_p, P(DeviceInfo)]),
     "nx_engine_bind_device": (C.c_int, [C.c_void_p, C.c_void_p]),
     "nx_device_weight": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, sz, P(sz)]),
     "nx_device_forward": (C.c_int, [C.c_void_p, P(BatchDesc), P(C.c_int32), P(C.c_float), P(C.c_double)]),
+    "nx_device_launch": (C.c_int, [C.c_void_p, P(BatchDesc)]),
+    "nx_device_wait": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_int32), P(C.c_float), P(C.c_double)]),
     "nx_dev_malloc": (C.c_int, [sz, P(C.c_void_p)]),
     "nx_dev_free": (C.c_int, [C.c_void_p]),
     "nx_dev_h2d": (C.c_int, [C.c_void_p, C.c_void_p, sz]),

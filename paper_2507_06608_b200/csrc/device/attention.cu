@@ -462,6 +462,7 @@ cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                          static_cast<int>(smem));
     configured = true;
   }
+  ++g_kernel_launches;
   prefill_attn_kernel<<<dim3(n_work, g.n_kv_heads), kThreadsAttn, smem, s>>>(
       g, qkv, kplane, vplane, seqs, work, pages, out);
   return cudaGetLastError();
@@ -496,10 +497,12 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   }
   const int per = (tiles + splits - 1) / splits;
   splits = std::max(1, (tiles + per - 1) / per);
+  ++g_kernel_launches;
   decode_attn_kernel<<<dim3(n_seq * splits, g.n_kv_heads), kThreadsAttn, smem, s>>>(
       g, qkv, kplane, vplane, seqs, pages, splits, per, out, part_o, part_ml);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || splits == 1) return e;
+  ++g_kernel_launches;
   decode_combine_kernel<<<dim3(n_seq, g.n_heads), kHD, 0, s>>>(g, seqs, splits, part_o, part_ml,
                                                                out);
   return cudaGetLastError();

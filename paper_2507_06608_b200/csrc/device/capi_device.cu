@@ -95,8 +95,7 @@ int nx_device_weight(const nx_device* dev, int32_t tensor, int32_t layer, void* 
   });
 }
 
-int nx_device_forward(nx_device* dev, const nx_batch_desc* b, int32_t* sampled, float* logits,
-                      double* device_ms) {
+int nx_device_launch(nx_device* dev, const nx_batch_desc* b) {
   return dguard([&] {
     nxb::ExecBatch eb;
     eb.lane_kind = b->lane == 1 ? NX_LANE_DECODE : NX_LANE_PREFILL;
@@ -121,8 +120,15 @@ int nx_device_forward(nx_device* dev, const nx_batch_desc* b, int32_t* sampled, 
       eb.members.push_back(m);
     }
     if (b->lane == 0 && any_decode && any_prefill) eb.lane_kind = NX_LANE_MIXED;
-    const int slot = b->lane == 1 ? nxb::kLaneDecode : nxb::kLanePrefill;
-    dev->m->launch(slot, eb);
+    dev->m->launch(b->lane == 1 ? nxb::kLaneDecode : nxb::kLanePrefill, eb);
+    return NX_OK;
+  });
+}
+
+int nx_device_wait(nx_device* dev, int32_t lane, int32_t* sampled, float* logits,
+                   double* device_ms) {
+  return dguard([&] {
+    const int slot = lane == 1 ? nxb::kLaneDecode : nxb::kLanePrefill;
     dev->m->wait(slot);
     const std::vector<int32_t>& s = dev->m->sampled(slot);
     if (sampled) std::memcpy(sampled, s.data(), s.size() * 4);
@@ -130,6 +136,28 @@ int nx_device_forward(nx_device* dev, const nx_batch_desc* b, int32_t* sampled, 
     if (device_ms) *device_ms = dev->m->device_ms(slot);
     return NX_OK;
   });
+}
+
+int nx_device_forward(nx_device* dev, const nx_batch_desc* b, int32_t* sampled, float* logits,
+                      double* device_ms) {
+  const int rc = nx_device_launch(dev, b);
+  if (rc != NX_OK) return rc;
+  return nx_device_wait(dev, b->lane, sampled, logits, device_ms);
+}
+
+int nx_device_set_profiling(nx_device* dev, int32_t sample_every) {
+  dev->m->set_profiling(sample_every);
+  return NX_OK;
+}
+
+int nx_device_kernel_stats(const nx_device* dev, nx_kernel_stats* out) {
+  *out = dev->m->kernel_stats();
+  return NX_OK;
+}
+
+int nx_device_reset_kernel_stats(nx_device* dev) {
+  dev->m->reset_kernel_stats();
+  return NX_OK;
 }
 
 int nx_dev_malloc(size_t bytes, void** p) { return cuda_rc(cudaMalloc(p, bytes)); }

@@ -10,6 +10,9 @@
 
 namespace nxd {
 
+// Count of kernels launched by this library (host-side, all streams).
+extern unsigned long long g_kernel_launches;
+
 // ---- GEMM (gemm_tc.cu) -------------------------------------------------------
 enum EpiMode {
   kEpiStore = 0,         // out = acc (bf16)

@@ -331,6 +331,7 @@ cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmPa
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  ++g_kernel_launches;
   gemm_tc_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(tw, tx, p);
   return cudaGetLastError();
 }
@@ -389,6 +390,7 @@ cudaError_t gemm(const CUtensorMap& w_map, const CUtensorMap& x_map_for_bn, int 
   if (e != cudaSuccess || p.splits == 1) return e;
   const int out_cols = final_mode == kEpiSwiGLU ? rows / 2 : rows;
   const int work = tokens * (out_cols / 8);
+  ++g_kernel_launches;
   splitk_reduce_kernel<<<(work + 255) / 256, 256, 0, stream>>>(p, final_mode);
   return cudaGetLastError();
 }

@@ -9,6 +9,9 @@
 #include "device.cuh"
 
 namespace nxd {
+
+unsigned long long g_kernel_launches = 0;
+
 namespace {
 
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
@@ -171,6 +174,7 @@ __global__ void fill_random_kernel(__nv_bfloat16* p, size_t n, uint64_t seed, fl
 cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int hidden,
                   __nv_bfloat16* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  ++g_kernel_launches;
   embed_kernel<<<n, 128, 0, s>>>(tokens, table, hidden, out);
   return cudaGetLastError();
 }
@@ -178,6 +182,7 @@ cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int 
 cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows, int n, int hidden,
                     const __nv_bfloat16* w, float eps, __nv_bfloat16* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  ++g_kernel_launches;
   rmsnorm_kernel<<<n, 256, 0, s>>>(x, rows, hidden, w, eps, out);
   return cudaGetLastError();
 }
@@ -187,6 +192,7 @@ cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* pos,
                           int head_dim, int page_tokens, __nv_bfloat16* kplane,
                           __nv_bfloat16* vplane, cudaStream_t s) {
   if (n_tokens == 0) return cudaSuccess;
+  ++g_kernel_launches;
   rope_kv_kernel<<<n_tokens, 256, 0, s>>>(qkv, pos, slot, inv_freq, n_heads, n_kv_heads, head_dim,
                                           page_tokens, kplane, vplane);
   return cudaGetLastError();
@@ -194,6 +200,7 @@ cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* pos,
 
 cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  ++g_kernel_launches;
   argmax_kernel<<<n, 1024, 0, s>>>(logits, vocab, out);
   return cudaGetLastError();
 }

@@ -88,8 +88,9 @@ void Partitions::init(int device, bool enable) {
 // total_sm and the layout whose lane size is nearest wins (ties: fewer SMs).
 Partitions::Pick Partitions::pick(int lane_kind, int sm_pct) const {
   Pick p;
-  if (lane_kind == 3 /*mixed*/ || !enabled) {
-    p.stream = lane_kind == 3 ? full_stream : plain_stream[lane_kind == 2 ? 1 : 0];
+  if (lane_kind == 3 /*mixed*/ || !enabled || sm_pct >= 100) {
+    p.stream = (lane_kind == 3 || (enabled && sm_pct >= 100)) ? full_stream
+                                                               : plain_stream[lane_kind == 2 ? 1 : 0];
     p.sm_count = total_sm;
     p.layout = -1;
     return p;
@@ -240,6 +241,8 @@ void LaneWs::init(Model* m, int max_tokens) {
   ck(cudaMallocHost(&out_host, static_cast<size_t>(T) * 4), "pinned out");
   ck(cudaEventCreate(&ev_start), "event");
   ck(cudaEventCreate(&ev_end), "event");
+  ev_pool.resize(2048);
+  for (auto& e : ev_pool) ck(cudaEventCreate(&e), "event");
   for (int i = 0; i < 4; ++i) {
     const uint32_t bn = 32u << i;
     if (!encode_kmajor(&map_h[i], h, T, a.hidden, static_cast<size_t>(a.hidden) * 2, bn) ||
@@ -307,6 +310,8 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   int t = 0, pg = 0, ns = 0, nw = 0;
   ws.dec_seq_count = 0;
   ws.max_dec_kv = 0;
+  ws.dec_kv_tokens = ws.pre_kv_tokens = ws.pre_pairs = 0;
+  ws.is_decode_lane = slot == nxb::kLaneDecode;
   // decode members (q_len == 1) first in the seq table so the decode kernel
   // can take a prefix; the batch lists them first already.
   for (int i = 0; i < n_seq; ++i) {
@@ -328,7 +333,11 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
       if (i != ws.dec_seq_count) throw std::runtime_error("decode members must come first");
       ws.dec_seq_count++;
       ws.max_dec_kv = std::max(ws.max_dec_kv, s.kv_len);
+      ws.dec_kv_tokens += s.kv_len;
     } else {
+      const double st = static_cast<double>(m.start_pos), q = m.n_tokens;
+      ws.pre_kv_tokens += s.kv_len;
+      ws.pre_pairs += q * st + q * (q + 1) / 2;
       for (int r = 0; r < m.n_tokens * group; r += 64) work[nw++] = make_int2(i, r);
     }
     t += m.n_tokens;
@@ -339,6 +348,9 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   ws.n_work = nw;
   ws.n_sample = ns;
   cudaStream_t s = ws.stream;
+  ws.prof = sample_every_ > 0 && (ws.batch_counter++ % static_cast<uint64_t>(sample_every_)) == 0;
+  ws.recs.clear();
+  ws.ev_used = 0;
   ck(cudaEventRecord(ws.ev_start, s), "event record");
   ck(cudaMemcpyAsync(ws.meta_dev, hp, off, cudaMemcpyHostToDevice, s), "meta h2d");
   const uint8_t* dp = ws.meta_dev;
@@ -359,11 +371,31 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
 
 void Model::forward(LaneWs& ws) {
   cudaStream_t s = ws.stream;
+  // Sampled profiling: an event pair around each launch, with its
+  // algorithmic bytes / FLOPs, folded into kstats_ when the batch finishes.
+  auto timed = [&](int kind, double bytes, double flops, auto&& fn) {
+    if (!ws.prof || ws.ev_used + 2 > ws.ev_pool.size()) {
+      fn();
+      return;
+    }
+    cudaEvent_t a = ws.ev_pool[ws.ev_used++], b = ws.ev_pool[ws.ev_used++];
+    cudaEventRecord(a, s);
+    fn();
+    cudaEventRecord(b, s);
+    ws.recs.push_back({kind, a, b, bytes, flops});
+  };
   const int T = ws.tokens;
+  const double Td = T;
   const int d = a_.hidden;
   const int bn = gemm_pick_bn(T);
   const int bi = bn_index(bn);
   const int sm = ws.sm_count;
+  const int gk = ws.is_decode_lane ? NX_K_GEMM_DECODE : NX_K_GEMM_PREFILL;
+  // algorithmic GEMM traffic: weights once + activations in + out (+ residual)
+  auto gbytes = [&](double rows, double K, double out_b, bool res) {
+    return rows * K * 2 + Td * K * 2 + Td * rows * out_b + (res ? Td * rows * 2 : 0);
+  };
+  auto gflops = [&](double rows, double K) { return 2.0 * Td * rows * K; };
   AttnGeom g;
   g.n_heads = a_.n_heads;
   g.n_kv_heads = a_.n_kv_heads;
@@ -373,47 +405,77 @@ void Model::forward(LaneWs& ws) {
   g.qkv_stride = qkv_rows_;
   g.out_stride = attn_cols_;
   g.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(a_.head_dim));
-  ck(embed(ws.d_tok, T, emb_, d, ws.x, s), "embed");
+  const double kvtok = 2.0 * a_.n_kv_heads * a_.head_dim * 2;  // K+V bytes per token per layer
+  const double qo = 2.0 * attn_cols_ * 2;                       // q in + out per token
+  timed(NX_K_OTHER, Td * d * 2 + Td * 4, 0, [&] { ck(embed(ws.d_tok, T, emb_, d, ws.x, s), "embed"); });
   for (int l = 0; l < a_.n_layers; ++l) {
     const LayerW& w = layers_[l];
     __nv_bfloat16* kplane = kv_ + (2 * static_cast<size_t>(l)) * plane_elems_;
     __nv_bfloat16* vplane = kplane + plane_elems_;
-    ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
-    ck(gemm(w.m_qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore, ws.qkv,
-            qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
-       "qkv gemm");
-    ck(rope_kv_write(ws.qkv, T, ws.d_pos, ws.d_slot, inv_freq_, a_.n_heads, a_.n_kv_heads,
-                     a_.head_dim, cfg_.page_tokens, kplane, vplane, s),
-       "rope");
+    timed(NX_K_OTHER, Td * d * 4, 0, [&] {
+      ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
+    });
+    timed(gk, gbytes(qkv_rows_, d, 2, false), gflops(qkv_rows_, d), [&] {
+      ck(gemm(w.m_qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
+              ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+         "qkv gemm");
+    });
+    timed(NX_K_OTHER, Td * qkv_rows_ * 4, 0, [&] {
+      ck(rope_kv_write(ws.qkv, T, ws.d_pos, ws.d_slot, inv_freq_, a_.n_heads, a_.n_kv_heads,
+                       a_.head_dim, cfg_.page_tokens, kplane, vplane, s),
+         "rope");
+    });
     if (ws.dec_seq_count > 0)
-      ck(decode_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.dec_seq_count, ws.max_dec_kv,
-                          ws.d_pages, ws.attn, ws.part_o, ws.part_ml, ws.part_cap, sm, s),
-         "decode attention");
+      timed(NX_K_ATTN_DECODE, ws.dec_kv_tokens * kvtok + ws.dec_seq_count * qo,
+            4.0 * ws.dec_kv_tokens * attn_cols_, [&] {
+              ck(decode_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.dec_seq_count,
+                                  ws.max_dec_kv, ws.d_pages, ws.attn, ws.part_o, ws.part_ml,
+                                  ws.part_cap, sm, s),
+                 "decode attention");
+            });
     if (ws.n_work > 0)
-      ck(prefill_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.d_work, ws.n_work, ws.d_pages,
-                           ws.attn, s),
-         "prefill attention");
-    ck(gemm(w.m_o, ws.map_attn[bi], bn, d, T, attn_cols_, kEpiResidual, ws.x, d, nullptr, ws.x, d,
-            ws.ws, ws.ws_bytes, sm, s),
-       "o gemm");
-    ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
-    ck(gemm(w.m_gate_up, ws.map_h[bi], bn, 2 * a_.ffn, T, d, kEpiSwiGLU, ws.act, a_.ffn, nullptr,
-            nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
-       "gate/up gemm");
-    ck(gemm(w.m_down, ws.map_act[bi], bn, d, T, a_.ffn, kEpiResidual, ws.x, d, nullptr, ws.x, d,
-            ws.ws, ws.ws_bytes, sm, s),
-       "down gemm");
+      timed(NX_K_ATTN_PREFILL, ws.pre_kv_tokens * kvtok + (Td - ws.dec_seq_count) * qo,
+            4.0 * ws.pre_pairs * attn_cols_, [&] {
+              ck(prefill_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.d_work, ws.n_work,
+                                   ws.d_pages, ws.attn, s),
+                 "prefill attention");
+            });
+    timed(gk, gbytes(d, attn_cols_, 2, true), gflops(d, attn_cols_), [&] {
+      ck(gemm(w.m_o, ws.map_attn[bi], bn, d, T, attn_cols_, kEpiResidual, ws.x, d, nullptr, ws.x,
+              d, ws.ws, ws.ws_bytes, sm, s),
+         "o gemm");
+    });
+    timed(NX_K_OTHER, Td * d * 4, 0, [&] {
+      ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
+    });
+    timed(gk, gbytes(2.0 * a_.ffn, d, 1, false), gflops(2.0 * a_.ffn, d), [&] {
+      ck(gemm(w.m_gate_up, ws.map_h[bi], bn, 2 * a_.ffn, T, d, kEpiSwiGLU, ws.act, a_.ffn, nullptr,
+              nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+         "gate/up gemm");
+    });
+    timed(gk, gbytes(d, a_.ffn, 2, true), gflops(d, a_.ffn), [&] {
+      ck(gemm(w.m_down, ws.map_act[bi], bn, d, T, a_.ffn, kEpiResidual, ws.x, d, nullptr, ws.x, d,
+              ws.ws, ws.ws_bytes, sm, s),
+         "down gemm");
+    });
   }
   // lm_head over the sampled rows, in chunks of the logits buffer.
   ws.d_out_tokens = ws.logits_tokens_dev();
   for (int r0 = 0; r0 < ws.n_sample; r0 += ws.sample_cap) {
     const int n = std::min(ws.sample_cap, ws.n_sample - r0);
-    ck(rmsnorm(ws.x, ws.d_rows + r0, n, d, final_norm_, a_.rms_eps, ws.hs, s), "final norm");
+    const double nd = n;
+    timed(NX_K_OTHER, nd * d * 4, 0, [&] {
+      ck(rmsnorm(ws.x, ws.d_rows + r0, n, d, final_norm_, a_.rms_eps, ws.hs, s), "final norm");
+    });
     const int sbn = gemm_pick_bn(n);
-    ck(gemm(m_lm_, ws.map_hs[bn_index(sbn)], sbn, a_.vocab, n, d, kEpiF32, ws.logits, a_.vocab,
-            nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
-       "lm_head gemm");
-    ck(argmax_rows(ws.logits, n, a_.vocab, ws.d_out_tokens + r0, s), "argmax");
+    timed(gk, static_cast<double>(a_.vocab) * d * 2 + nd * d * 2 + nd * a_.vocab * 4,
+          2.0 * nd * a_.vocab * d, [&] {
+            ck(gemm(m_lm_, ws.map_hs[bn_index(sbn)], sbn, a_.vocab, n, d, kEpiF32, ws.logits,
+                    a_.vocab, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+               "lm_head gemm");
+          });
+    timed(NX_K_OTHER, nd * a_.vocab * 4, 0,
+          [&] { ck(argmax_rows(ws.logits, n, a_.vocab, ws.d_out_tokens + r0, s), "argmax"); });
   }
 }
 
@@ -444,10 +506,25 @@ void Model::wait(int slot) {
 
 void Model::finish(LaneWs& ws) {
   ws.pending = false;
+  kstats_.batches += 1;
   ws.sampled.assign(ws.out_host, ws.out_host + ws.n_sample);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ws.ev_start, ws.ev_end);
   ws.last_ms = ms;
+  if (ws.prof) {
+    for (const auto& r : ws.recs) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      kstats_.ms[r.kind] += t;
+      kstats_.bytes[r.kind] += r.bytes;
+      kstats_.flops[r.kind] += r.flops;
+      kstats_.launches[r.kind] += 1;
+    }
+    kstats_.batches_sampled += 1;
+    kstats_.batch_ms_sampled += ms;
+    ws.recs.clear();
+    ws.prof = false;
+  }
 }
 
 void Model::copy_logits(int slot, float* host, size_t n_floats) {

@@ -75,6 +75,19 @@ struct LaneWs {
   bool pending = false;
   std::vector<int32_t> sampled;
   float last_ms = 0.f;
+  // sampled per-kernel-class profiling
+  struct ProfRec {
+    int kind;
+    cudaEvent_t a, b;
+    double bytes, flops;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<ProfRec> recs;
+  bool prof = false;
+  uint64_t batch_counter = 0;
+  double dec_kv_tokens = 0, pre_kv_tokens = 0, pre_pairs = 0;
+  bool is_decode_lane = false;
 };
 
 struct LayerW {
@@ -103,6 +116,13 @@ class Model : public nxb::Executor {
   uint64_t kv_bytes() const { return kv_bytes_; }
   int last_layout(int slot) const { return lanes_[slot].layout; }
   int last_sm_count(int slot) const { return lanes_[slot].sm_count; }
+  void set_profiling(int every) { sample_every_ = every; }
+  nx_kernel_stats kernel_stats() const {
+    nx_kernel_stats k = kstats_;
+    k.kernel_launches = g_kernel_launches;
+    return k;
+  }
+  void reset_kernel_stats() { kstats_ = nx_kernel_stats{}; }
 
  private:
   friend struct LaneWs;
@@ -124,6 +144,8 @@ class Model : public nxb::Executor {
   size_t plane_elems_ = 0;
   uint64_t weight_bytes_ = 0, kv_bytes_ = 0;
   LaneWs lanes_[2];
+  int sample_every_ = 0;
+  nx_kernel_stats kstats_{};
 };
 
 }  // namespace nxd

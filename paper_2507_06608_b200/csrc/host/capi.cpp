@@ -86,6 +86,10 @@ struct nx_controller {
   Controller c;
 };
 
+namespace {
+thread_local nx_cost_ext g_ext{};
+}
+
 extern "C" {
 
 const char* nx_last_error(void) { return g_last_error.c_str(); }
@@ -172,7 +176,7 @@ int nx_phase_latency_isolated(const nx_op_workload* ops, size_t n, double share,
                               const nx_gpu_spec* g, const nx_kernel_profile* p,
                               nx_breakdown* out) {
   return guarded([&] {
-    *out = isolated(to_ops(ops, n), share, *g, *p);
+    *out = isolated(to_ops(ops, n), share, *g, *p, &g_ext);
     return NX_OK;
   });
 }
@@ -190,16 +194,27 @@ int nx_decode_latency_contended(const nx_op_workload* dops, size_t nd, double sh
                                 const nx_gpu_spec* g, const nx_kernel_profile* p,
                                 nx_breakdown* out) {
   return guarded([&] {
-    *out = decode_contended(to_ops(dops, nd), share, pbd, to_ops(pops, np), *g, *p);
+    *out = decode_contended(to_ops(dops, nd), share, pbd, to_ops(pops, np), *g, *p, &g_ext);
     return NX_OK;
   });
+}
+
+int nx_set_cost_ext(const nx_cost_ext* ext) {
+  if (ext) {
+    for (double s : ext->bw_sat)
+      if (ext->enabled && !(s > 0.0 && s <= 1.0)) return fail(NX_EINVAL, "bw_sat must lie in (0, 1]");
+    g_ext = *ext;
+  } else {
+    g_ext = nx_cost_ext{};
+  }
+  return NX_OK;
 }
 
 double nx_min_phase_latency(const nx_op_workload* ops, size_t n, const nx_gpu_spec* g,
                             const nx_kernel_profile* p) {
   if (n == 0) return 0.0;  // a vacuous phase imposes no constraint
   try {
-    return isolated(to_ops(ops, n), 1.0, *g, *p).total_s;
+    return isolated(to_ops(ops, n), 1.0, *g, *p, &g_ext).total_s;
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return -1.0;

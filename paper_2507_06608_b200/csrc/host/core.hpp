@@ -63,17 +63,19 @@ OpList mixed_ops(const nx_model_config& m, const Chunk* chunks, size_t n, const 
 
 // ---- cost model (reference costmodel.cpp) ---------------------------------
 double compute_latency(double flops, double share, const nx_saturation_curve& c, double peak);
-// decode_bw <= 0 means "all operators at peak bandwidth".
+// decode_bw <= 0 means "all operators at peak bandwidth". ext == nullptr or
+// !ext->enabled is the reference model exactly.
 nx_breakdown breakdown(const OpList& ops, double share, const nx_gpu_spec& g,
-                       const nx_kernel_profile& p, double decode_bw);
+                       const nx_kernel_profile& p, double decode_bw,
+                       const nx_cost_ext* ext = nullptr);
 inline nx_breakdown isolated(const OpList& ops, double share, const nx_gpu_spec& g,
-                             const nx_kernel_profile& p) {
-  return breakdown(ops, share, g, p, 0.0);
+                             const nx_kernel_profile& p, const nx_cost_ext* ext = nullptr) {
+  return breakdown(ops, share, g, p, 0.0, ext);
 }
 double effective_decode_bw(double p_attn, double m_d, double m_p1, double m_p2, double peak);
 nx_breakdown decode_contended(const OpList& dec, double share, const nx_breakdown* pre_bd,
                               const OpList& pre, const nx_gpu_spec& g,
-                              const nx_kernel_profile& p);
+                              const nx_kernel_profile& p, const nx_cost_ext* ext = nullptr);
 
 // ---- controller (reference optimizer.cpp) ---------------------------------
 int select_mode(int64_t used, int64_t cap, double frac);

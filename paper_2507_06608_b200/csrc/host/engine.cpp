@@ -197,11 +197,12 @@ struct ModelCtx {
   const OpList* ops;
   const nx_gpu_spec* gpu;
   const nx_kernel_profile* prof;
+  const nx_cost_ext* ext;
 };
 // Planning latencies are isolated (simulator.cpp:299-314).
 double latency_at(void* user, int32_t pct) {
   const ModelCtx* m = static_cast<const ModelCtx*>(user);
-  return isolated(*m->ops, pct / 100.0, *m->gpu, *m->prof).total_s;
+  return isolated(*m->ops, pct / 100.0, *m->gpu, *m->prof, m->ext).total_s;
 }
 }  // namespace
 
@@ -212,7 +213,7 @@ int Engine::decide(int launching, const OpList& launching_ops) {
   const OpList dec = decode_.busy ? decode_.ops
                                   : (launching == NX_PHASE_DECODE ? launching_ops
                                                                   : provisional_decode());
-  ModelCtx pc{&pre, &cfg_.gpu, &cfg_.profile}, dc{&dec, &cfg_.gpu, &cfg_.profile};
+  ModelCtx pc{&pre, &cfg_.gpu, &cfg_.profile, &cfg_.ext}, dc{&dec, &cfg_.gpu, &cfg_.profile, &cfg_.ext};
   const nx_phase_model pm{pre.empty() ? 0 : 1, latency_at, &pc};
   const nx_phase_model dm{dec.empty() ? 0 : 1, latency_at, &dc};
   const nx_decision d = ctl_.decide(kv_used_, cfg_.gpu.kv_capacity_bytes, pm, dm);
@@ -320,8 +321,8 @@ bool Engine::launch_decode() {
   if (dynamic_) r_p = decide(NX_PHASE_DECODE, ops);
   const double share = (100 - r_p) / 100.0;
   decode_.bd = prefill_.busy ? decode_contended(ops, share, &prefill_.bd, prefill_.ops,
-                                                cfg_.gpu, cfg_.profile)
-                             : isolated(ops, share, cfg_.gpu, cfg_.profile);
+                                                cfg_.gpu, cfg_.profile, &cfg_.ext)
+                             : isolated(ops, share, cfg_.gpu, cfg_.profile, &cfg_.ext);
   decode_.dec = std::move(plan.members);
   decode_.pre.clear();
   decode_.ops = ops;
@@ -340,7 +341,7 @@ bool Engine::launch_prefill() {
   OpList ops = prefill_ops(cfg_.model, ch.data(), ch.size());
   int r_p = ctl_.state().r_p;
   if (dynamic_) r_p = decide(NX_PHASE_PREFILL, ops);
-  prefill_.bd = isolated(ops, r_p / 100.0, cfg_.gpu, cfg_.profile);
+  prefill_.bd = isolated(ops, r_p / 100.0, cfg_.gpu, cfg_.profile, &cfg_.ext);
   prefill_.pre = std::move(kept);
   prefill_.dec.clear();
   prefill_.ops = ops;
@@ -365,7 +366,7 @@ bool Engine::launch_mixed() {
   const auto ch = chunks_of(pre);
   const auto ctx = decode_ctx(dec);
   OpList ops = mixed_ops(cfg_.model, ch.data(), ch.size(), ctx.data(), ctx.size());
-  prefill_.bd = isolated(ops, 1.0, cfg_.gpu, cfg_.profile);
+  prefill_.bd = isolated(ops, 1.0, cfg_.gpu, cfg_.profile, &cfg_.ext);
   prefill_.dec = std::move(dec);
   prefill_.pre = std::move(pre);
   prefill_.ops = ops;

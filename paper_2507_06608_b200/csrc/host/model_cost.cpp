@@ -253,8 +253,9 @@ double compute_latency(double flops, double share, const nx_saturation_curve& c,
 
 // Sum over operators of max(compute, memory) (costmodel.cpp:18-41).
 nx_breakdown breakdown(const OpList& ops, double share, const nx_gpu_spec& g,
-                       const nx_kernel_profile& p, double decode_bw) {
+                       const nx_kernel_profile& p, double decode_bw, const nx_cost_ext* ext) {
   if (ops.empty()) throw InvalidArg("phase latency: empty operator list");
+  const bool use_ext = ext != nullptr && ext->enabled != 0;
   nx_breakdown out{};
   out.n_ops = ops.n;
   for (int i = 0; i < ops.n; ++i) {
@@ -263,7 +264,12 @@ nx_breakdown breakdown(const OpList& ops, double share, const nx_gpu_spec& g,
     nx_op_latency& o = out.per_op[i];
     o.kind = w.kind;
     o.compute_s = compute_latency(w.flops, share, curve_of(p, w.kind), g.peak_compute);
-    o.mem_s = w.mem_bytes / (contended ? decode_bw : g.peak_bandwidth);
+    double bw = contended ? decode_bw : g.peak_bandwidth;
+    if (use_ext) {
+      const double sat = ext->bw_sat[w.kind];
+      if (sat > 0 && share < sat) bw = bw * (share / sat);  // SM-share-limited HBM bandwidth
+    }
+    o.mem_s = w.mem_bytes / bw;
     o.memory_bound = o.mem_s > o.compute_s ? 1 : 0;
     const double t = o.compute_s < o.mem_s ? o.mem_s : o.compute_s;  // std::max order
     out.total_s += t;
@@ -287,8 +293,8 @@ double effective_decode_bw(double p_attn, double m_d, double m_p1, double m_p2, 
 // prefill breakdown.
 nx_breakdown decode_contended(const OpList& dec, double share, const nx_breakdown* pre_bd,
                               const OpList& pre, const nx_gpu_spec& g,
-                              const nx_kernel_profile& p) {
-  if (pre_bd == nullptr) return isolated(dec, share, g, p);
+                              const nx_kernel_profile& p, const nx_cost_ext* ext) {
+  if (pre_bd == nullptr) return isolated(dec, share, g, p, ext);
   const double p_attn = pre_bd->total_s <= 0 ? 0.0 : pre_bd->attn_mem_time_s / pre_bd->total_s;
   double m_p1 = 0, m_p2 = 0, m_d = 0;
   for (int i = 0; i < pre.n; ++i) {
@@ -301,7 +307,7 @@ nx_breakdown decode_contended(const OpList& dec, double share, const nx_breakdow
     if (dec.op[i].kind == NX_OP_ATTN_DECODE) m_d += dec.op[i].kv_bytes;
   const double bw = m_d > 0 ? effective_decode_bw(p_attn, m_d, m_p1, m_p2, g.peak_bandwidth)
                             : g.peak_bandwidth;
-  return breakdown(dec, share, g, p, bw);
+  return breakdown(dec, share, g, p, bw, ext);
 }
 
 }  // namespace nxb

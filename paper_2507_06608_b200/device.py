@@ -8,7 +8,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi
-from ._dev_abi import Arch, BatchDesc, DeviceConfig, DeviceInfo
+from ._dev_abi import Arch, BatchDesc, DeviceConfig, DeviceInfo, KernelStats
 
 W_EMBED, W_ATTN_NORM, W_QKV, W_QKV_BIAS, W_O, W_FFN_NORM, W_GATE_UP, W_DOWN, W_FINAL_NORM, W_LM_HEAD = range(10)
 
@@ -80,6 +80,17 @@ class Device:
         _check(lib().nx_device_get_info(self.handle, C.byref(i)))
         return i
 
+    def set_profiling(self, sample_every: int) -> None:
+        _check(lib().nx_device_set_profiling(self.handle, sample_every))
+
+    def kernel_stats(self) -> KernelStats:
+        k = KernelStats()
+        _check(lib().nx_device_kernel_stats(self.handle, C.byref(k)))
+        return k
+
+    def reset_kernel_stats(self) -> None:
+        _check(lib().nx_device_reset_kernel_stats(self.handle))
+
     def weight(self, tensor: int, layer: int = 0) -> np.ndarray:
         n = C.c_size_t()
         _check(lib().nx_device_weight(self.handle, tensor, layer, None, 0, C.byref(n)))
@@ -87,6 +98,33 @@ class Device:
         if n.value:
             _check(lib().nx_device_weight(self.handle, tensor, layer, out.ctypes.data, n.value, C.byref(n)))
         return bf16_to_f32(out)
+
+    def _desc(self, members, lane, sm_pct):
+        n = len(members)
+        nt = (C.c_int32 * n)(*[len(m["tokens"]) for m in members])
+        sp = (C.c_int64 * n)(*[m["start"] for m in members])
+        sa = (C.c_int32 * n)(*[1 if m.get("sample", True) else 0 for m in members])
+        toks = [t for m in members for t in m["tokens"]]
+        tk = (C.c_int32 * max(1, len(toks)))(*toks)
+        npg = (C.c_int32 * n)(*[len(m["pages"]) for m in members])
+        pgs = [p for m in members for p in m["pages"]]
+        pg = (C.c_int32 * max(1, len(pgs)))(*pgs)
+        keep = (nt, sp, sa, tk, npg, pg)
+        return BatchDesc(lane, sm_pct, n, 0, nt, sp, sa, tk, npg, pg), keep, int(sum(sa))
+
+    def launch(self, members, lane=0, sm_pct=100):
+        """Asynchronous launch (returns immediately); pair with wait(lane)."""
+        b, keep, ns = self._desc(members, lane, sm_pct)
+        _check(lib().nx_device_launch(self.handle, C.byref(b)))
+        self._pending = getattr(self, "_pending", {})
+        self._pending[lane] = ns
+
+    def wait(self, lane):
+        ns = self._pending.pop(lane)
+        out = (C.c_int32 * max(1, ns))()
+        ms = C.c_double()
+        _check(lib().nx_device_wait(self.handle, lane, out, None, C.byref(ms)))
+        return list(out[:ns]), ms.value
 
     def forward(self, members, lane=0, sm_pct=100, want_logits=False):
         """members: list of dict(tokens=[...], start=int, pages=[...], sample=bool)."""

@@ -298,3 +298,31 @@ def test_empty_trace(nx, ref):
     mine = nx.run(cfg, [])
     theirs = ref.run(cfg, [])
     assert mine.event_log == theirs["event_log"] == ""
+
+
+def test_cost_ext_disabled_is_reference_and_port_mirrors_enabled(nx, ref):
+    """The flagged bandwidth extension: off == reference exactly; on, the
+    product engine and the Python port still agree byte for byte."""
+    from oracle.engine_port import run_port
+    m = nx.model_preset("8b")
+    g = nx.gpu_spec(148, 1.3e15, 5.5e12, 150 << 30)
+    trace = nx.workload_trace("sharegpt", 25.0, 150, 4)
+    off = nx.sim_config(m, g)
+    assert nx.run(off, trace).event_log == ref.run(off, trace)["event_log"]
+    on = nx.sim_config(m, g, bw_sat=[0.55, 0.7, 0.6, 0.55, 0.55])
+    r = nx.run(on, trace)
+    ev, dec = run_port(on, trace)
+    assert r.event_log == ev and r.decision_log == dec
+    # the extension changes the split: decode gets far more than 1-8 % of SMs
+    applied = [int(l.split("\t")[4]) for l in r.decision_log.splitlines()[1:]]
+    assert min(applied) < 90
+    # standalone cost queries honour nx_set_cost_ext
+    ops = nx.decode_op_workloads(m, [600] * 64)
+    prof = nx.lib().nx_kernel_profile_default()
+    base = nx.phase_latency_isolated(ops, 0.2, g, prof).total_s
+    nx.set_cost_ext([0.6] * 5)
+    try:
+        slow = nx.phase_latency_isolated(ops, 0.2, g, prof).total_s
+    finally:
+        nx.set_cost_ext(None)
+    assert slow > 2.5 * base
