@@ -1,7 +1,9 @@
 // Device half of the C-ABI (include/nexus_b200.h, "device executor" section).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <memory>
 #include <string>
 
@@ -81,16 +83,8 @@ int nx_engine_bind_device(nx_engine* eng, nx_device* dev) {
 int nx_device_weight(const nx_device* dev, int32_t tensor, int32_t layer, void* host,
                      size_t cap_bytes, size_t* bytes) {
   return dguard([&] {
-    size_t elems = 0;
-    const __nv_bfloat16* p = dev->m->weight_ptr(tensor, layer, &elems);
-    if (!p && elems) return dfail(NX_EINVAL, "unknown tensor/layer");
-    *bytes = elems * 2;
-    if (!host) return NX_OK;
-    if (cap_bytes < elems * 2) return dfail(NX_EINVAL, "buffer too small");
-    if (elems) {
-      const int rc = cuda_rc(cudaMemcpy(host, p, elems * 2, cudaMemcpyDeviceToHost));
-      if (rc) return rc;
-    }
+    *bytes = dev->m->weight_to_host(tensor, layer, nullptr, 0);
+    if (host) dev->m->weight_to_host(tensor, layer, host, cap_bytes);
     return NX_OK;
   });
 }
@@ -175,10 +169,17 @@ int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32
                int32_t sm_count, int32_t splits, int32_t iters, float* ms) {
   return dguard([&] {
     const int bn = nxd::gemm_pick_bn(tokens);
-    CUtensorMap wm, xm;
-    if (!nxd::encode_kmajor(&wm, w, rows, K, static_cast<uint64_t>(K) * 2, 128) ||
-        !nxd::encode_kmajor(&xm, x, tokens, K, static_cast<uint64_t>(K) * 2, bn))
+    CUtensorMap xm;
+    if (!nxd::encode_kmajor(&xm, x, tokens, K, static_cast<uint64_t>(K) * 2, bn))
       return dfail(NX_ERUNTIME, "tensor map encode failed");
+    __nv_bfloat16* wp = nullptr;
+    int prc = cuda_rc(cudaMalloc(&wp, nxd::packed_weight_elems(rows, K) * 2));
+    if (prc) return prc;
+    prc = cuda_rc(nxd::pack_weights(static_cast<const __nv_bfloat16*>(w), wp, rows, K, nullptr));
+    if (prc) {
+      cudaFree(wp);
+      return prc;
+    }
     int dev = 0;
     cudaGetDevice(&dev);
     int n_sm = 0;
@@ -188,25 +189,30 @@ int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32
     const size_t ws_bytes = 256u << 20;
     int rc = cuda_rc(cudaMalloc(&ws, ws_bytes));
     if (rc) return rc;
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    rc = cuda_rc(cudaMemset(ws, 0, nxd::gemm_counter_bytes()));
+    if (rc) return rc;
+    // Per-launch device time: an event pair around every launch, median
+    // reported (host enqueue gaps between launches are excluded).
     const int n = iters > 0 ? iters : 1;
+    std::vector<cudaEvent_t> ev(2 * n);
+    for (auto& e : ev) cudaEventCreate(&e);
     cudaError_t err = cudaSuccess;
-    cudaEventRecord(e0, nullptr);
-    for (int i = 0; i < n && err == cudaSuccess; ++i)
-      err = nxd::gemm(wm, xm, bn, rows, tokens, K, mode, out, ldo,
+    for (int i = 0; i < n && err == cudaSuccess; ++i) {
+      cudaEventRecord(ev[2 * i], nullptr);
+      err = nxd::gemm(wp, xm, bn, rows, tokens, K, mode, out, ldo,
                       static_cast<const __nv_bfloat16*>(bias),
                       static_cast<const __nv_bfloat16*>(residual), ldr, ws, ws_bytes, sm_count,
                       nullptr, splits);
-    cudaEventRecord(e1, nullptr);
-    if (err == cudaSuccess) err = cudaEventSynchronize(e1);
-    float t = 0.f;
-    cudaEventElapsedTime(&t, e0, e1);
-    if (ms) *ms = t;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+      cudaEventRecord(ev[2 * i + 1], nullptr);
+    }
+    if (err == cudaSuccess) err = cudaDeviceSynchronize();
+    std::vector<float> t(n, 0.f);
+    for (int i = 0; i < n; ++i) cudaEventElapsedTime(&t[i], ev[2 * i], ev[2 * i + 1]);
+    std::sort(t.begin(), t.end());
+    if (ms) *ms = t[n / 2] * n;  // median per launch, scaled so ms / iters = median
+    for (auto& e : ev) cudaEventDestroy(e);
     cudaFree(ws);
+    cudaFree(wp);
     return cuda_rc(err);
   });
 }

@@ -34,16 +34,30 @@ struct GemmParams {
   const __nv_bfloat16* residual;
   int ldr;
   float* ws;
+  int streamk;     // 1: stream-K partition of the (tile, k-block) iterations
+  int max_pieces;  // stream-K: partial slots per tile
+  int bn;          // token tile (for the stream-K fix-up)
+  int* tile_count; // stream-K: per-tile arrival counters (zero between launches)
 };
 
 int gemm_pick_bn(int tokens);
 // y[tokens, rows] = epi(x[tokens, K] . w[rows, K]^T). `x_map` must have been
 // encoded with box rows == bn. sm_count sizes the persistent grid (the lane's
 // green-context partition); force_splits > 0 overrides the K-split choice.
-cudaError_t gemm(const CUtensorMap& w_map, const CUtensorMap& x_map, int bn, int rows, int tokens,
+// Weights are used in the packed tile layout (pack_weights): each 128 x 64
+// tile is a contiguous, pre-swizzled 16 KB chunk streamed by cp.async.bulk.
+size_t packed_weight_elems(int rows, int K);
+cudaError_t pack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int K,
+                         cudaStream_t s);
+cudaError_t unpack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int K,
+                           cudaStream_t s);
+// ws must start with gemm_counter_bytes() of zeroed int counters (kept zero
+// by the kernel itself between launches on the same stream).
+cudaError_t gemm(const __nv_bfloat16* w_packed, const CUtensorMap& x_map, int bn, int rows, int tokens,
                  int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
                  const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
                  cudaStream_t stream, int force_splits = 0);
+constexpr size_t gemm_counter_bytes() { return 64 * 1024; }
 
 // K-major bf16 [rows, cols] tensor map with a 64 x box_rows, 128B-swizzled box.
 bool encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,

@@ -52,6 +52,47 @@ struct Unit {
   int m_blk, n_blk, split;
 };
 
+// Packed weight layout: 128-row blocks in pairs, [pair][kb][2][128][64],
+// each 128 x 64 tile stored as its 128B-swizzled shared-memory image (16 B
+// chunk c of row r at chunk position c ^ (r & 7)), so a stage is one
+// contiguous 16 KB cp.async.bulk and pairs of row blocks are adjacent.
+__host__ __device__ __forceinline__ size_t packed_tile_offset(int m_blk, int kb, int num_kb) {
+  return ((static_cast<size_t>(m_blk >> 1) * num_kb + kb) * 2 + (m_blk & 1)) * (kBM * kBK);
+}
+
+__global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                    int rows, int K, int pad_rows) {
+  const int num_kb = K / kBK;
+  const size_t n_chunks = static_cast<size_t>(pad_rows) * (K / 8);
+  for (size_t c = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; c < n_chunks;
+       c += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(c / (K / 8));
+    const int kc = static_cast<int>(c % (K / 8));  // 16 B chunk along K
+    const int kb = kc >> 3, ch = kc & 7;
+    const int m_blk = row / kBM, r = row % kBM;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < rows) v = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(row) * K + kc * 8);
+    __nv_bfloat16* t = dst + packed_tile_offset(m_blk, kb, num_kb) + r * kBK + ((ch ^ (r & 7)) << 3);
+    *reinterpret_cast<uint4*>(t) = v;
+  }
+}
+
+__global__ void unpack_weights_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                      int rows, int K) {
+  const int num_kb = K / kBK;
+  const size_t n_chunks = static_cast<size_t>(rows) * (K / 8);
+  for (size_t c = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; c < n_chunks;
+       c += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(c / (K / 8));
+    const int kc = static_cast<int>(c % (K / 8));
+    const int kb = kc >> 3, ch = kc & 7;
+    const int m_blk = row / kBM, r = row % kBM;
+    *reinterpret_cast<uint4*>(dst + static_cast<size_t>(row) * K + kc * 8) =
+        *reinterpret_cast<const uint4*>(src + packed_tile_offset(m_blk, kb, num_kb) + r * kBK +
+                                        ((ch ^ (r & 7)) << 3));
+  }
+}
+
 __device__ __forceinline__ Unit unit_of(int u, const GemmParams& p) {
   Unit r;
   r.split = u % p.splits;
@@ -61,9 +102,159 @@ __device__ __forceinline__ Unit unit_of(int u, const GemmParams& p) {
   return r;
 }
 
+struct Work {
+  int m_blk, n_blk, kb0, kb1;
+  int slot;      // stream-K: partial slot (tile * max_pieces + piece); split-K: split index
+  bool partial;  // true: write fp32 partials for a fix-up pass
+};
+
+// This CTA's work items, in the same order for every warp role.
+//  * data-parallel / split-K: units blockIdx.x, +gridDim.x, ...
+//  * stream-K: the contiguous iteration range [c*I/G, (c+1)*I/G) over the
+//    flattened (tile, k-block) space, cut at tile boundaries into pieces.
+struct WorkIter {
+  const GemmParams& p;
+  int u = 0;
+  long long it = 0, end = 0, total = 0;
+  __device__ explicit WorkIter(const GemmParams& pp) : p(pp) {
+    if (p.streamk) {
+      total = static_cast<long long>(p.n_mblk) * p.n_nblk * p.num_kb;
+      it = total * blockIdx.x / gridDim.x;
+      end = total * (blockIdx.x + 1) / gridDim.x;
+    } else {
+      u = blockIdx.x;
+    }
+  }
+  __device__ bool next(Work& w) {
+    if (p.streamk) {
+      if (it >= end) return false;
+      const int tile = static_cast<int>(it / p.num_kb);
+      w.kb0 = static_cast<int>(it % p.num_kb);
+      w.kb1 = static_cast<int>(min(static_cast<long long>(p.num_kb), w.kb0 + (end - it)));
+      w.n_blk = tile % p.n_nblk;
+      w.m_blk = tile / p.n_nblk;
+      w.partial = !(w.kb0 == 0 && w.kb1 == p.num_kb);
+      w.slot = -1;
+      if (w.partial) {
+        const long long it0 = static_cast<long long>(tile) * p.num_kb;
+        const int first = static_cast<int>(((it0 + 1) * gridDim.x - 1) / total);
+        w.slot = tile * p.max_pieces + (static_cast<int>(blockIdx.x) - first);
+      }
+      it += w.kb1 - w.kb0;
+      return true;
+    }
+    if (u >= p.n_mblk * p.n_nblk * p.splits) return false;
+    const Unit x = unit_of(u, p);
+    w.m_blk = x.m_blk;
+    w.n_blk = x.n_blk;
+    w.kb0 = x.split * p.kb_per_split;
+    w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
+    w.partial = p.splits > 1;
+    w.slot = x.split;
+    u += gridDim.x;
+    return true;
+  }
+};
+
+// Stream-K fix-up by the last arriving piece of a split tile: the 128
+// epilogue threads publish their fp32 partial, count the tile's arrivals
+// with one atomic, and the last CTA folds every piece of the tile and
+// applies the epilogue (classic threadfence reduction; no extra launch).
+template <int BN>
+__device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& w, int et, int* s_flag) {
+  const int tile = w.m_blk * p.n_nblk + w.n_blk;
+  const long long total = static_cast<long long>(p.n_mblk) * p.n_nblk * p.num_kb;
+  const long long it0 = static_cast<long long>(tile) * p.num_kb;
+  const int first = static_cast<int>(((it0 + 1) * gridDim.x - 1) / total);
+  const int last = static_cast<int>(((it0 + p.num_kb) * gridDim.x - 1) / total);
+  const int pieces = last - first + 1;
+  __threadfence();
+  named_bar_sync(1, kEpiThreads);
+  if (et == 0) {
+    const int prev = atomicAdd(&p.tile_count[tile], 1);
+    *s_flag = prev == pieces - 1;
+    if (prev == pieces - 1) p.tile_count[tile] = 0;  // ready for the next launch
+  }
+  named_bar_sync(1, kEpiThreads);
+  if (!*s_flag) return;
+  __threadfence();
+  const int tok_base = w.n_blk * BN;
+  const int n_tok = min(BN, p.tokens - tok_base);
+  const float4* base =
+      reinterpret_cast<const float4*>(p.ws + static_cast<size_t>(tile) * p.max_pieces * BN * kBM);
+  constexpr int kSlot4 = BN * kBM / 4;  // float4 per piece slot
+  // Each thread owns kPer float4 positions (coalesced: position = et + 128 i);
+  // pieces are the outer loop so every pass issues kPer independent loads.
+  constexpr int kPer = 8;
+  const int n4 = n_tok * (kBM / 4);
+  for (int chunk = 0; chunk < n4; chunk += kEpiThreads * kPer) {
+    float4 acc[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < pieces; ++q) {
+      float4 v[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int pos = chunk + et + i * kEpiThreads;
+        v[i] = pos < n4 ? __ldcg(base + q * kSlot4 + pos) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        acc[i].x += v[i].x;
+        acc[i].y += v[i].y;
+        acc[i].z += v[i].z;
+        acc[i].w += v[i].w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int pos = chunk + et + i * kEpiThreads;
+      if (pos >= n4) continue;
+      const int j = pos / (kBM / 4), c = (pos % (kBM / 4)) * 4;  // token, feature in tile
+      const int t = tok_base + j;
+      if (p.mode == kEpiSwiGLU) {
+        if (c >= 64) continue;  // gate half drives the output; up half read below
+        float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < pieces; ++q) {
+          const float4 b = __ldcg(base + q * kSlot4 + pos + 16);
+          u.x += b.x, u.y += b.y, u.z += b.z, u.w += b.w;
+        }
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo +
+                             w.m_blk * 64 + c;
+        *reinterpret_cast<__nv_bfloat162*>(dst) =
+            __floats2bfloat162_rn(silu(acc[i].x) * u.x, silu(acc[i].y) * u.y);
+        *reinterpret_cast<__nv_bfloat162*>(dst + 2) =
+            __floats2bfloat162_rn(silu(acc[i].z) * u.z, silu(acc[i].w) * u.w);
+        continue;
+      }
+      const int f = w.m_blk * kBM + c;
+      if (p.mode == kEpiF32) {
+        *reinterpret_cast<float4*>(static_cast<float*>(p.out) + static_cast<size_t>(t) * p.ldo + f) =
+            acc[i];
+        continue;
+      }
+      float o0 = acc[i].x, o1 = acc[i].y, o2 = acc[i].z, o3 = acc[i].w;
+      if (p.mode == kEpiBias || p.mode == kEpiBiasResidual) {
+        const __nv_bfloat162 b01 = *reinterpret_cast<const __nv_bfloat162*>(p.bias + f);
+        const __nv_bfloat162 b23 = *reinterpret_cast<const __nv_bfloat162*>(p.bias + f + 2);
+        o0 += __low2float(b01), o1 += __high2float(b01), o2 += __low2float(b23), o3 += __high2float(b23);
+      }
+      if (p.mode == kEpiResidual || p.mode == kEpiBiasResidual) {
+        const __nv_bfloat16* rp = p.residual + static_cast<size_t>(t) * p.ldr + f;
+        const __nv_bfloat162 r01 = *reinterpret_cast<const __nv_bfloat162*>(rp);
+        const __nv_bfloat162 r23 = *reinterpret_cast<const __nv_bfloat162*>(rp + 2);
+        o0 += __low2float(r01), o1 += __high2float(r01), o2 += __low2float(r23), o3 += __high2float(r23);
+      }
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo + f;
+      *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(o0, o1);
+      *reinterpret_cast<__nv_bfloat162*>(dst + 2) = __floats2bfloat162_rn(o2, o3);
+    }
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+    gemm_tc_kernel(const __nv_bfloat16* __restrict__ wpack, const __grid_constant__ CUtensorMap tx,
                    GemmParams p) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
@@ -75,10 +266,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   if (warp == 0 && elect_one()) {
-    tma_prefetch(&tw);
     tma_prefetch(&tx);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -95,7 +286,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int units = p.n_mblk * p.n_nblk * p.splits;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -103,15 +293,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t w_policy = policy_evict_first();  // weights stream once
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = unit_of(u, p);
-        const int kb0 = w.split * p.kb_per_split;
-        const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb) {
+      WorkIter wi(p);
+      Work w;
+      while (wi.next(w)) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStage;
           mbar_expect_tx(&full[stage], C::kStage);
-          tma_load_2d_hint(&tw, &full[stage], sa, kb * kBK, w.m_blk * kBM, w_policy);
+          // weight tile = one contiguous 16 KB pre-swizzled chunk (see pack_weights)
+          bulk_load(sa, wpack + packed_tile_offset(w.m_blk, kb, p.num_kb), kABytes, &full[stage],
+                    w_policy);
           tma_load_2d(&tx, &full[stage], sa + kABytes, kb * kBK, w.n_blk * BN);
           if (++stage == C::kStages) {
             stage = 0;
@@ -126,10 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-      const Unit w = unit_of(u, p);
-      const int kb0 = w.split * p.kb_per_split;
-      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+    WorkIter wi(p);
+    Work w;
+    for (; wi.next(w); ++local) {
+      const int kb0 = w.kb0, kb1 = w.kb1;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -161,8 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int et = threadIdx.x - 64;
     const int lane = lane_id();
     int local = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-      const Unit w = unit_of(u, p);
+    WorkIter wi(p);
+    Work w;
+    for (; wi.next(w); ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -177,7 +369,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) s_epi[j * kBM + q * 32 + lane] = __uint_as_float(r[j]);
         named_bar_sync(1, kEpiThreads);
-        if (p.mode == kEpiSwiGLU) {
+        if (w.partial) {
+          // fp32 partials: stream-K slot [BN tokens][128] or split-K plane
+          const int g = et & 31;
+#pragma unroll
+          for (int pass = 0; pass < 8; ++pass) {
+            const int j = pass * 4 + (et >> 5);
+            const int t = tok0 + j;
+            if (t < p.tokens) {
+              const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
+              float* dst = p.streamk
+                               ? p.ws + (static_cast<size_t>(w.slot) * BN + c0 + j) * kBM + g * 4
+                               : p.ws + (static_cast<size_t>(w.slot) * p.tokens + t) * p.rows + f0 + g * 4;
+              *reinterpret_cast<float4*>(dst) = v;
+            }
+          }
+        } else if (p.mode == kEpiSwiGLU) {
           // rows 0-63 of the tile are gate features, 64-127 the matching up features
           const int g = et & 7;
 #pragma unroll
@@ -195,18 +402,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) +
                                    static_cast<size_t>(t) * p.ldo + w.m_blk * 64 + g * 8;
               *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(o);
-            }
-          }
-        } else if (p.mode == kEpiPartial) {
-          const int g = et & 31;
-#pragma unroll
-          for (int pass = 0; pass < 8; ++pass) {
-            const int j = pass * 4 + (et >> 5);
-            const int t = tok0 + j;
-            if (t < p.tokens) {
-              const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
-              float* dst = p.ws + (static_cast<size_t>(w.split) * p.tokens + t) * p.rows + f0 + g * 4;
-              *reinterpret_cast<float4*>(dst) = v;
             }
           }
         } else if (p.mode == kEpiF32) {
@@ -258,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (p.streamk && w.partial) streamk_arrive<BN>(p, w, et, s_flag);
     }
   }
   __syncthreads();
@@ -321,7 +517,7 @@ __global__ void splitk_reduce_kernel(GemmParams p, int final_mode) {
 }
 
 template <int BN>
-cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, int grid,
+cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const GemmParams& p, int grid,
                       cudaStream_t s) {
   using C = Cfg<BN>;
   static bool configured = false;
@@ -338,11 +534,33 @@ cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmPa
 
 }  // namespace
 
+size_t packed_weight_elems(int rows, int K) {
+  const int blocks = (rows + kBM - 1) / kBM;
+  return static_cast<size_t>((blocks + 1) & ~1) * kBM * K;
+}
+
+cudaError_t pack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int K,
+                         cudaStream_t s) {
+  if (K % kBK) return cudaErrorInvalidValue;
+  const int blocks = (rows + kBM - 1) / kBM;
+  const int pad_rows = ((blocks + 1) & ~1) * kBM;
+  ++g_kernel_launches;
+  pack_weights_kernel<<<1184, 256, 0, s>>>(src, dst, rows, K, pad_rows);
+  return cudaGetLastError();
+}
+
+cudaError_t unpack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int K,
+                           cudaStream_t s) {
+  ++g_kernel_launches;
+  unpack_weights_kernel<<<1184, 256, 0, s>>>(src, dst, rows, K);
+  return cudaGetLastError();
+}
+
 int gemm_pick_bn(int tokens) {
   return tokens <= 32 ? 32 : tokens <= 64 ? 64 : tokens <= 128 ? 128 : 256;
 }
 
-cudaError_t gemm(const CUtensorMap& w_map, const CUtensorMap& x_map_for_bn, int bn, int rows,
+cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, int bn, int rows,
                  int tokens, int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
                  const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
                  cudaStream_t stream, int force_splits) {
@@ -361,24 +579,40 @@ cudaError_t gemm(const CUtensorMap& w_map, const CUtensorMap& x_map_for_bn, int 
   p.bias = bias;
   p.residual = residual;
   p.ldr = ldr;
-  p.ws = ws;
-  // K splits: fill the partition when there are fewer tiles than SMs,
-  // keeping >= 4 K blocks per split and the partials inside the workspace.
+  p.bn = bn;
+  // ws layout: [int tile counters | fp32 partials]
+  p.tile_count = reinterpret_cast<int*>(ws);
+  p.ws = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + gemm_counter_bytes()) : nullptr;
+  ws_bytes = ws_bytes > gemm_counter_bytes() ? ws_bytes - gemm_counter_bytes() : 0;
   const int tiles = p.n_mblk * p.n_nblk;
-  int splits = 1;
+  const long long iters = static_cast<long long>(tiles) * p.num_kb;
+  int grid;
+  p.splits = 1;
+  p.kb_per_split = p.num_kb;
+  p.streamk = 0;
   if (force_splits > 0) {
-    splits = force_splits;
-  } else if (tiles < sm_count && ws != nullptr) {
-    splits = std::min((sm_count + tiles - 1) / tiles, std::max(1, p.num_kb / 4));
-    splits = std::min(splits, 16);
+    // explicit split-K (tests / experiments)
+    p.kb_per_split = (p.num_kb + force_splits - 1) / force_splits;
+    p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+    if (static_cast<size_t>(p.splits) * tokens * rows * 4 > ws_bytes) return cudaErrorInvalidValue;
+    grid = std::max(1, std::min(tiles * p.splits, sm_count));
+  } else if (tokens <= 256 && ws != nullptr && tiles % sm_count != 0 &&
+             static_cast<size_t>(tiles) * 4 <= gemm_counter_bytes()) {
+    // Stream-K: equal (tile, k-block) ranges per CTA remove the wave tail
+    // of decode-shaped launches (weight streaming: every CTA busy to the end).
+    const int G = static_cast<int>(std::min<long long>(sm_count, iters));
+    const long long per_min = iters / G;
+    p.max_pieces = static_cast<int>((p.num_kb + per_min - 1) / per_min) + 1;
+    const size_t need = static_cast<size_t>(tiles) * p.max_pieces * bn * kBM * 4;
+    if (need <= ws_bytes && tiles < 8 * G) {
+      p.streamk = 1;
+      grid = G;
+    } else {
+      grid = std::max(1, std::min(tiles, sm_count));
+    }
+  } else {
+    grid = std::max(1, std::min(tiles, sm_count));
   }
-  while (splits > 1 && static_cast<size_t>(splits) * tokens * rows * 4 > ws_bytes) --splits;
-  p.kb_per_split = (p.num_kb + splits - 1) / splits;
-  p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
-  const int final_mode = mode;
-  if (p.splits > 1) p.mode = kEpiPartial;
-  const int units = tiles * p.splits;
-  const int grid = std::max(1, std::min(units, sm_count));
   cudaError_t e;
   switch (bn) {
     case 32: e = launch_bn<32>(w_map, x_map_for_bn, p, grid, stream); break;
@@ -387,11 +621,12 @@ cudaError_t gemm(const CUtensorMap& w_map, const CUtensorMap& x_map_for_bn, int 
     case 256: e = launch_bn<256>(w_map, x_map_for_bn, p, grid, stream); break;
     default: return cudaErrorInvalidValue;
   }
-  if (e != cudaSuccess || p.splits == 1) return e;
-  const int out_cols = final_mode == kEpiSwiGLU ? rows / 2 : rows;
+  if (e != cudaSuccess) return e;
+  if (p.streamk || p.splits == 1) return cudaSuccess;
+  const int out_cols = mode == kEpiSwiGLU ? rows / 2 : rows;
   const int work = tokens * (out_cols / 8);
   ++g_kernel_launches;
-  splitk_reduce_kernel<<<(work + 255) / 256, 256, 0, stream>>>(p, final_mode);
+  splitk_reduce_kernel<<<(work + 255) / 256, 256, 0, stream>>>(p, mode);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <initializer_list>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -167,34 +168,43 @@ void Model::alloc_weights() {
   auto next_seed = [&]() { return seed = seed * 6364136223846793005ULL + 1442695040888963407ULL; };
   const float g = cfg_.weight_gain > 0 ? cfg_.weight_gain : 1.0f;
   auto uni = [&](size_t k) { return g * std::sqrt(3.0f / static_cast<float>(k)); };
-  auto make = [&](size_t n, float scale, float offset) {
+  // staging buffer for the logical (row-major) random init before packing
+  const size_t max_mat = std::max({static_cast<size_t>(qkv_rows_) * d, d * attn_cols_,
+                                   2 * static_cast<size_t>(a_.ffn) * d,
+                                   static_cast<size_t>(a_.vocab) * d});
+  __nv_bfloat16* stage = nullptr;
+  ck(cudaMalloc(&stage, max_mat * 2), "weight staging");
+  auto plain = [&](size_t n, float scale, float offset) {
     __nv_bfloat16* p = dalloc_bf16(n);
     ck(fill_random(p, n, next_seed(), scale, offset, nullptr), "init weights");
     weight_bytes_ += n * 2;
     return p;
   };
-  emb_ = make(static_cast<size_t>(a_.vocab) * d, 1.0f, 0.f);
+  auto packed = [&](int rows, int K, float scale) {
+    const size_t n = static_cast<size_t>(rows) * K;
+    ck(fill_random(stage, n, next_seed(), scale, 0.f, nullptr), "init weights");
+    __nv_bfloat16* p = dalloc_bf16(packed_weight_elems(rows, K));
+    ck(pack_weights(stage, p, rows, K, nullptr), "pack weights");
+    weight_bytes_ += n * 2;
+    return p;
+  };
+  emb_ = plain(static_cast<size_t>(a_.vocab) * d, 1.0f, 0.f);
   layers_.resize(L);
   for (size_t l = 0; l < L; ++l) {
     LayerW& w = layers_[l];
-    w.attn_norm = make(d, 0.1f, 1.0f);
-    w.qkv = make(static_cast<size_t>(qkv_rows_) * d, uni(d), 0.f);
-    w.qkv_bias = a_.qkv_bias ? make(qkv_rows_, 0.1f, 0.f) : nullptr;
-    w.o = make(d * attn_cols_, uni(attn_cols_), 0.f);
-    w.ffn_norm = make(d, 0.1f, 1.0f);
-    w.gate_up = make(2 * static_cast<size_t>(a_.ffn) * d, uni(d), 0.f);
-    w.down = make(d * a_.ffn, uni(a_.ffn) * 2.0f, 0.f);
-    if (!encode_kmajor(&w.m_qkv, w.qkv, qkv_rows_, d, d * 2, 128) ||
-        !encode_kmajor(&w.m_o, w.o, d, attn_cols_, attn_cols_ * 2, 128) ||
-        !encode_kmajor(&w.m_gate_up, w.gate_up, 2 * a_.ffn, d, d * 2, 128) ||
-        !encode_kmajor(&w.m_down, w.down, d, a_.ffn, static_cast<size_t>(a_.ffn) * 2, 128))
-      throw std::runtime_error("cuTensorMapEncodeTiled failed (weights)");
+    w.attn_norm = plain(d, 0.1f, 1.0f);
+    w.qkv = packed(qkv_rows_, static_cast<int>(d), uni(d));
+    w.qkv_bias = a_.qkv_bias ? plain(qkv_rows_, 0.1f, 0.f) : nullptr;
+    w.o = packed(static_cast<int>(d), attn_cols_, uni(attn_cols_));
+    w.ffn_norm = plain(d, 0.1f, 1.0f);
+    w.gate_up = packed(2 * a_.ffn, static_cast<int>(d), uni(d));
+    w.down = packed(static_cast<int>(d), a_.ffn, uni(a_.ffn) * 2.0f);
   }
-  final_norm_ = make(d, 0.1f, 1.0f);
+  final_norm_ = plain(d, 0.1f, 1.0f);
   const float lm_gain = cfg_.lm_head_gain > 0 ? cfg_.lm_head_gain : 1.0f;
-  lm_head_ = make(static_cast<size_t>(a_.vocab) * d, lm_gain * std::sqrt(3.0f / d), 0.f);
-  if (!encode_kmajor(&m_lm_, lm_head_, a_.vocab, d, d * 2, 128))
-    throw std::runtime_error("cuTensorMapEncodeTiled failed (lm_head)");
+  lm_head_ = packed(a_.vocab, static_cast<int>(d), lm_gain * std::sqrt(3.0f / d));
+  ck(cudaDeviceSynchronize(), "weights");
+  cudaFree(stage);
 }
 
 void Model::alloc_kv() {
@@ -229,6 +239,7 @@ void LaneWs::init(Model* m, int max_tokens) {
   logits = static_cast<float*>(alloc(static_cast<size_t>(sample_cap) * a.vocab * 4));
   ws_bytes = 96u << 20;
   ws = static_cast<float*>(alloc(ws_bytes));
+  ck(cudaMemset(ws, 0, gemm_counter_bytes()), "zero gemm counters");
   part_cap = static_cast<size_t>(8) << 20;  // floats
   part_o = static_cast<float*>(alloc(part_cap * 4));
   part_ml = static_cast<float*>(alloc(part_cap / a.head_dim * 2 * 4 + 1024));
@@ -416,7 +427,7 @@ void Model::forward(LaneWs& ws) {
       ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
     });
     timed(gk, gbytes(qkv_rows_, d, 2, false), gflops(qkv_rows_, d), [&] {
-      ck(gemm(w.m_qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
+      ck(gemm(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
               ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
          "qkv gemm");
     });
@@ -441,7 +452,7 @@ void Model::forward(LaneWs& ws) {
                  "prefill attention");
             });
     timed(gk, gbytes(d, attn_cols_, 2, true), gflops(d, attn_cols_), [&] {
-      ck(gemm(w.m_o, ws.map_attn[bi], bn, d, T, attn_cols_, kEpiResidual, ws.x, d, nullptr, ws.x,
+      ck(gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, kEpiResidual, ws.x, d, nullptr, ws.x,
               d, ws.ws, ws.ws_bytes, sm, s),
          "o gemm");
     });
@@ -449,12 +460,12 @@ void Model::forward(LaneWs& ws) {
       ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
     });
     timed(gk, gbytes(2.0 * a_.ffn, d, 1, false), gflops(2.0 * a_.ffn, d), [&] {
-      ck(gemm(w.m_gate_up, ws.map_h[bi], bn, 2 * a_.ffn, T, d, kEpiSwiGLU, ws.act, a_.ffn, nullptr,
+      ck(gemm(w.gate_up, ws.map_h[bi], bn, 2 * a_.ffn, T, d, kEpiSwiGLU, ws.act, a_.ffn, nullptr,
               nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
          "gate/up gemm");
     });
     timed(gk, gbytes(d, a_.ffn, 2, true), gflops(d, a_.ffn), [&] {
-      ck(gemm(w.m_down, ws.map_act[bi], bn, d, T, a_.ffn, kEpiResidual, ws.x, d, nullptr, ws.x, d,
+      ck(gemm(w.down, ws.map_act[bi], bn, d, T, a_.ffn, kEpiResidual, ws.x, d, nullptr, ws.x, d,
               ws.ws, ws.ws_bytes, sm, s),
          "down gemm");
     });
@@ -470,7 +481,7 @@ void Model::forward(LaneWs& ws) {
     const int sbn = gemm_pick_bn(n);
     timed(gk, static_cast<double>(a_.vocab) * d * 2 + nd * d * 2 + nd * a_.vocab * 4,
           2.0 * nd * a_.vocab * d, [&] {
-            ck(gemm(m_lm_, ws.map_hs[bn_index(sbn)], sbn, a_.vocab, n, d, kEpiF32, ws.logits,
+            ck(gemm(lm_head_, ws.map_hs[bn_index(sbn)], sbn, a_.vocab, n, d, kEpiF32, ws.logits,
                     a_.vocab, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
                "lm_head gemm");
           });
@@ -533,23 +544,41 @@ void Model::copy_logits(int slot, float* host, size_t n_floats) {
   ck(cudaMemcpy(host, ws.logits, want * 4, cudaMemcpyDeviceToHost), "logits d2h");
 }
 
-const __nv_bfloat16* Model::weight_ptr(int tensor, int layer, size_t* elems) const {
+size_t Model::weight_to_host(int tensor, int layer, void* host, size_t cap) const {
   const size_t d = a_.hidden;
   if (tensor != 0 && tensor != 8 && tensor != 9 && (layer < 0 || layer >= a_.n_layers))
-    return nullptr;
+    throw std::invalid_argument("unknown layer");
+  const __nv_bfloat16* p = nullptr;
+  size_t elems = 0;
+  int rows = 0, K = 0;  // > 0: packed matrix
   switch (tensor) {
-    case 0: *elems = static_cast<size_t>(a_.vocab) * d; return emb_;
-    case 1: *elems = d; return layers_[layer].attn_norm;
-    case 2: *elems = static_cast<size_t>(qkv_rows_) * d; return layers_[layer].qkv;
-    case 3: *elems = a_.qkv_bias ? qkv_rows_ : 0; return layers_[layer].qkv_bias;
-    case 4: *elems = d * attn_cols_; return layers_[layer].o;
-    case 5: *elems = d; return layers_[layer].ffn_norm;
-    case 6: *elems = 2 * static_cast<size_t>(a_.ffn) * d; return layers_[layer].gate_up;
-    case 7: *elems = d * a_.ffn; return layers_[layer].down;
-    case 8: *elems = d; return final_norm_;
-    case 9: *elems = static_cast<size_t>(a_.vocab) * d; return lm_head_;
-    default: return nullptr;
+    case 0: p = emb_; elems = static_cast<size_t>(a_.vocab) * d; break;
+    case 1: p = layers_[layer].attn_norm; elems = d; break;
+    case 2: p = layers_[layer].qkv; rows = qkv_rows_; K = static_cast<int>(d); break;
+    case 3: p = layers_[layer].qkv_bias; elems = a_.qkv_bias ? qkv_rows_ : 0; break;
+    case 4: p = layers_[layer].o; rows = static_cast<int>(d); K = attn_cols_; break;
+    case 5: p = layers_[layer].ffn_norm; elems = d; break;
+    case 6: p = layers_[layer].gate_up; rows = 2 * a_.ffn; K = static_cast<int>(d); break;
+    case 7: p = layers_[layer].down; rows = static_cast<int>(d); K = a_.ffn; break;
+    case 8: p = final_norm_; elems = d; break;
+    case 9: p = lm_head_; rows = a_.vocab; K = static_cast<int>(d); break;
+    default: throw std::invalid_argument("unknown tensor");
   }
+  if (rows) elems = static_cast<size_t>(rows) * K;
+  if (!host) return elems * 2;
+  if (cap < elems * 2) throw std::invalid_argument("buffer too small");
+  if (!elems) return 0;
+  if (!rows) {
+    ck(cudaMemcpy(host, p, elems * 2, cudaMemcpyDeviceToHost), "weight d2h");
+    return elems * 2;
+  }
+  __nv_bfloat16* tmp = nullptr;
+  ck(cudaMalloc(&tmp, elems * 2), "unpack staging");
+  ck(unpack_weights(p, tmp, rows, K, nullptr), "unpack");
+  const cudaError_t e = cudaMemcpy(host, tmp, elems * 2, cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  ck(e, "weight d2h");
+  return elems * 2;
 }
 
 }  // namespace nxd

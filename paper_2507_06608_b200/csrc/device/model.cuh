@@ -90,9 +90,9 @@ struct LaneWs {
   bool is_decode_lane = false;
 };
 
+// Projection weights are held in the packed tile layout (pack_weights).
 struct LayerW {
   __nv_bfloat16 *attn_norm, *qkv, *qkv_bias, *o, *ffn_norm, *gate_up, *down;
-  CUtensorMap m_qkv, m_o, m_gate_up, m_down;
 };
 
 class Model : public nxb::Executor {
@@ -110,7 +110,8 @@ class Model : public nxb::Executor {
   int32_t num_pages() const override { return cfg_.num_pages; }
 
   void copy_logits(int slot, float* host, size_t n_floats);
-  const __nv_bfloat16* weight_ptr(int tensor, int layer, size_t* elems) const;
+  // Logical (row-major) copy of a weight tensor into host memory.
+  size_t weight_to_host(int tensor, int layer, void* host, size_t cap) const;
   const Partitions& partitions() const { return parts_; }
   uint64_t weight_bytes() const { return weight_bytes_; }
   uint64_t kv_bytes() const { return kv_bytes_; }
@@ -138,7 +139,6 @@ class Model : public nxb::Executor {
   Partitions parts_;
   std::vector<void*> allocs_;
   __nv_bfloat16 *emb_ = nullptr, *final_norm_ = nullptr, *lm_head_ = nullptr, *kv_ = nullptr;
-  CUtensorMap m_lm_;
   std::vector<LayerW> layers_;
   float* inv_freq_ = nullptr;
   size_t plane_elems_ = 0;

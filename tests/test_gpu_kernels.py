@@ -90,3 +90,37 @@ def test_gemm_f32_logits(D):
     D.gemm(bx, bw, T, N, K, D.EPI_F32, bo, N)
     dev = bo.to_array((T, N), np.float32)
     np.testing.assert_allclose(dev, ref, rtol=1e-3, atol=1e-3 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("T,N,K,sms,mode", [(64, 28672, 4096, 70, "swiglu"), (64, 4096, 14336, 37, "residual"),
+                                            (17, 6144, 4096, 100, "bias"), (128, 1024, 512, 148, "f32"),
+                                            (1, 128256 // 8 * 8, 512, 148, "f32")])
+def test_gemm_streamk_partitions(D, T, N, K, sms, mode):
+    """Decode-shaped launches on partial SM counts take the stream-K path
+    (equal (tile, k-block) ranges per CTA + fix-up of split tiles)."""
+    rng = np.random.default_rng(T + sms)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    b, r = _rand(D, rng, (N,)), _rand(D, rng, (T, N))
+    xf, wf = D.bf16_to_f32(x), D.bf16_to_f32(w)
+    bx, bw, bb, br = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf.from_array(b), D.Buf.from_array(r)
+    if mode == "swiglu":
+        F = N // 2
+        w4 = wf.reshape(F // 64, 2, 64, K)
+        g, u = xf @ w4[:, 0].reshape(F, K).T, xf @ w4[:, 1].reshape(F, K).T
+        ref = g / (1 + np.exp(-g)) * u
+        bo = D.Buf(T * F * 2)
+        D.gemm(bx, bw, T, N, K, D.EPI_SWIGLU, bo, F, sm_count=sms)
+        _close(D.bf16_to_f32(bo.to_array((T, F), np.uint16)), ref)
+        return
+    base = xf @ wf.T
+    if mode == "f32":
+        bo = D.Buf(T * N * 4)
+        D.gemm(bx, bw, T, N, K, D.EPI_F32, bo, N, sm_count=sms)
+        np.testing.assert_allclose(bo.to_array((T, N), np.float32), base, rtol=1e-3,
+                                   atol=1e-3 * np.abs(base).max())
+        return
+    m = {"residual": D.EPI_RESIDUAL, "bias": D.EPI_BIAS}[mode]
+    ref = base + (D.bf16_to_f32(r) if mode == "residual" else D.bf16_to_f32(b))
+    bo = D.Buf(T * N * 2)
+    D.gemm(bx, bw, T, N, K, m, bo, N, bias=bb, residual=br, ldr=N, sm_count=sms)
+    _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), ref)

@@ -1,0 +1,97 @@
+// Streaming-bandwidth probe: how fast can one CTA per SM pull bytes from
+// HBM into shared memory on B200 with (a) 2D TMA boxes (64 x 128 rows,
+// 128B swizzle: the GEMM's weight tile) vs (b) 1D cp.async.bulk copies of
+// contiguous chunks (pre-packed weight tiles), for several stage counts and
+// SM counts. Consumer = an arrive on the empty barrier (no math).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d: %s\n", #x, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(su32(b)), "r"(c)); }
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t n) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(su32(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n@!p bra W_%=;\n}" :: "r"(su32(b)), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+               :: "r"(su32(dst)), "l"((uint64_t)m), "r"(su32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void bulk1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+
+// mode 0: 2D TMA 64x128 boxes; mode 1: 1D bulk chunk bytes
+__global__ void stream_kernel(const __grid_constant__ CUtensorMap map, const char* base, int mode, int stages,
+                              int chunk, long long total_chunks, int rows) {
+  extern __shared__ __align__(1024) char smem[];
+  uint64_t* full = (uint64_t*)(smem + stages * chunk);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  long long my0 = total_chunks * blockIdx.x / gridDim.x, my1 = total_chunks * (blockIdx.x + 1) / gridDim.x;
+  int stage = 0; uint32_t phase = 0;
+  long long issued = my0, done = my0;
+  // prime
+  for (int s = 0; s < stages && issued < my1; ++s, ++issued) {
+    mbar_expect(&full[s], chunk);
+    if (mode == 0) { long long kb = issued % 64, mb = issued / 64; tma2d(&map, &full[s], smem + s * chunk, (int)kb * 64, (int)(mb * 128) % rows); }
+    else bulk1d(smem + s * chunk, base + (issued * chunk) % (1ll << 33), chunk, &full[s]);
+  }
+  while (done < my1) {
+    mbar_wait(&full[stage], phase);
+    ++done;
+    if (issued < my1) {
+      mbar_expect(&full[stage], chunk);
+      if (mode == 0) { long long kb = issued % 64, mb = issued / 64; tma2d(&map, &full[stage], smem + stage * chunk, (int)kb * 64, (int)(mb * 128) % rows); }
+      else bulk1d(smem + stage * chunk, base + (issued * chunk) % (1ll << 33), chunk, &full[stage]);
+      ++issued;
+    }
+    if (++stage == stages) { stage = 0; phase ^= 1; }
+  }
+}
+
+int main() {
+  CK(cudaSetDevice(0));
+  const size_t bytes = 8ull << 30;
+  char* buf; CK(cudaMalloc(&buf, bytes)); CK(cudaMemset(buf, 1, bytes));
+  void* fn = nullptr; cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  auto encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  const int K = 4096; const int rows = (int)(bytes / (K * 2));
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}; cuuint64_t str[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {64, 128}; cuuint32_t es[2] = {1, 1};
+  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encode fail\n"); return 1; }
+  CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  struct Cfg { int mode, chunk, stages; };
+  std::vector<Cfg> cfgs = {{0, 16384, 4}, {0, 16384, 8}, {0, 16384, 12}, {1, 16384, 8}, {1, 16384, 12}, {1, 32768, 6}, {1, 65536, 3}};
+  const long long total_bytes = 2ll << 30;
+  for (auto c : cfgs) {
+    for (int sms : {8, 16, 32, 64, 96, 128, 148}) {
+      long long chunks = total_bytes / c.chunk;
+      if (sms <= 16) chunks /= 8;
+      int smem = c.stages * c.chunk + 1024;
+      stream_kernel<<<sms, 32, smem>>>(map, buf, c.mode, c.stages, c.chunk, chunks, rows);
+      CK(cudaEventRecord(e0));
+      for (int i = 0; i < 3; ++i) stream_kernel<<<sms, 32, smem>>>(map, buf, c.mode, c.stages, c.chunk, chunks, rows);
+      CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+      float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
+      double gbs = 3.0 * chunks * c.chunk / (ms * 1e-3) / 1e9;
+      printf("{\"mode\": \"%s\", \"chunk\": %d, \"stages\": %d, \"sms\": %d, \"GBps\": %.0f, \"per_sm\": %.1f}\n",
+             c.mode ? "bulk1d" : "tma2d", c.chunk, c.stages, sms, gbs, gbs / sms);
+    }
+  }
+  return 0;
+}

@@ -1,0 +1,24 @@
+"""One Llama-3.1-8B decode batch (B x ctx) and one prefill batch on chosen
+partitions, repeated: the target of ncu launch lists / captures."""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2507_06608_b200 import device as D
+B = int(os.environ.get("B", "64")); CTX = int(os.environ.get("CTX", "600"))
+DPCT = int(os.environ.get("DPCT", "100")); PPCT = int(os.environ.get("PPCT", "100"))
+REPS = int(os.environ.get("REPS", "3")); MODE = os.environ.get("MODE", "decode")
+dev = D.Device(D.arch_preset("llama3-8b"), num_pages=B * (CTX // 16 + 2) + 600)
+rng = np.random.default_rng(0)
+pp = CTX // 16 + 2
+Dm = [dict(tokens=[int(rng.integers(0, 1000))], start=CTX - 1, pages=list(range(i * pp, (i + 1) * pp))) for i in range(B)]
+P = [dict(tokens=rng.integers(0, 1000, 512).tolist(), start=0, pages=list(range(B * pp + 40 * i, B * pp + 40 * i + 33))) for i in range(4)]
+import time
+for r in range(REPS):
+    if MODE in ("decode", "both"):
+        t0 = time.perf_counter(); dev.launch(Dm, lane=1, sm_pct=DPCT); t1 = time.perf_counter()
+        _, ms = dev.wait(1); t2 = time.perf_counter()
+        print(f"decode device_ms {ms:.3f} host_enqueue_ms {1e3*(t1-t0):.3f} wall_ms {1e3*(t2-t0):.3f}", flush=True)
+    if MODE in ("prefill", "both"):
+        t0 = time.perf_counter(); dev.launch(P, lane=0, sm_pct=PPCT); t1 = time.perf_counter()
+        _, ms = dev.wait(0); t2 = time.perf_counter()
+        print(f"prefill device_ms {ms:.3f} host_enqueue_ms {1e3*(t1-t0):.3f} wall_ms {1e3*(t2-t0):.3f}", flush=True)
