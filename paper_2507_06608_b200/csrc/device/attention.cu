@@ -1,10 +1,11 @@
 // Paged attention over the device-resident block table.
 //
-// KV cache layout per layer: K and V planes of [page][kv_head][page_tokens][hd]
-// bf16, so one (page, kv head) is a contiguous 16 x 256 B = 4 KB run that
-// 16-byte cp.async loads stream at full coalescing. Tiles of 64 keys are
-// staged in XOR-swizzled shared memory (conflict-free ldmatrix), double
-// buffered so the next tile's loads overlap this tile's math.
+// KV cache layout per layer: K and V planes of [page][kv_head][16][hd] bf16,
+// written pre-swizzled (16 B chunk c of token row r stored at c ^ (r & 7)), so
+// one (page, kv head) is a contiguous 4 KB run that is *already* the
+// conflict-free shared-memory image: a 64-key tile is 4 + 4 cp.async.bulk
+// copies issued by one thread on an mbarrier, with no per-thread address math
+// (the 16 B-per-thread loader this replaced was instruction-bound at ~2 TB/s).
 //
 //  * prefill: CTA = (sequence, kv head, 64 query rows); a query row is a
 //    (token, head-in-GQA-group) pair so all G heads sharing a KV head reuse
@@ -32,21 +33,12 @@ constexpr int kHD = 128;        // head dim (all supported models)
 constexpr int kKT = 64;         // keys per staged tile
 constexpr int kRowsPF = 64;     // query rows per prefill CTA
 constexpr int kThreadsAttn = 128;
+constexpr int kStagesPF = 2;   // prefill: 2 x 32 KB KV stages (+16 KB Q staging)
+constexpr int kStagesDec = 3;  // decode: 3 x 32 KB in flight per CTA, 2 CTAs / SM
 
 // Swizzled offset (elements) of (row, col) in a [rows][128] bf16 tile.
 __device__ __forceinline__ int swz(int row, int col) {
   return row * kHD + ((((col >> 3) ^ (row & 7)) << 3) | (col & 7));
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-  const uint32_t d = smem_u32(dst);
-  const int n = valid ? 16 : 0;  // src-size 0 -> zero fill
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
@@ -72,23 +64,25 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Stages keys [key0, key0 + 64) of one kv head into a swizzled tile; rows
-// past kv_len (or past the block table) are zero-filled.
-__device__ __forceinline__ void load_kv_tile(__nv_bfloat16* dst, const __nv_bfloat16* plane,
-                                             const int32_t* pages, int kv_len, int key0, int kvh,
-                                             const AttnGeom& g) {
-  // 64 rows x 16 chunks of 16 B = 1024 chunks; 128 threads x 8.
+// One thread: bulk-copies the pages covering keys [key0, key0 + 64) of one
+// kv head (K and V) into a tile; completion on `bar`. Pages wholly past
+// kv_end are skipped (their smem keeps finite stale/zero data; masked).
+__device__ __forceinline__ void issue_kv_tile(__nv_bfloat16* sk, __nv_bfloat16* sv, uint64_t* bar,
+                                              const __nv_bfloat16* kplane,
+                                              const __nv_bfloat16* vplane, const int32_t* pages,
+                                              int kv_end, int key0, int kvh, const AttnGeom& g,
+                                              uint64_t policy) {
+  // Slots past kv_end re-load the last valid page: their keys are masked and
+  // the data is finite, so P * V stays exact without zero-filling smem.
+  const int last_page = pages[(kv_end - 1) >> 4];
+  mbar_expect_tx(bar, 4 * 2 * 4096);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int c = threadIdx.x + i * kThreadsAttn;
-    const int row = c >> 4, chunk = c & 15;
-    const int key = key0 + row;
-    const bool valid = key < kv_len;
-    const int page = valid ? pages[key / g.page_tokens] : 0;
-    const __nv_bfloat16* src =
-        plane + ((static_cast<size_t>(page) * g.n_kv_heads + kvh) * g.page_tokens +
-                 key % g.page_tokens) * kHD + chunk * 8;
-    cp_async16(dst + row * kHD + ((chunk ^ (row & 7)) << 3), valid ? src : plane, valid);
+  for (int p = 0; p < 4; ++p) {
+    const int key = key0 + p * 16;
+    const int page = key < kv_end ? pages[key >> 4] : last_page;
+    const size_t off = (static_cast<size_t>(page) * g.n_kv_heads + kvh) * (16 * kHD);
+    bulk_load(sk + p * 16 * kHD, kplane + off, 4096, bar, policy);
+    bulk_load(sv + p * 16 * kHD, vplane + off, 4096, bar, policy);
   }
 }
 
@@ -221,10 +215,12 @@ __global__ void __launch_bounds__(kThreadsAttn)
                         const __nv_bfloat16* __restrict__ vplane, const AttnSeq* __restrict__ seqs,
                         const int2* __restrict__ work, const int32_t* __restrict__ pages,
                         __nv_bfloat16* __restrict__ out) {
-  extern __shared__ __align__(128) uint8_t smem_attn[];
-  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_attn);  // [2][64][128]
-  __nv_bfloat16* sv = sk + 2 * kKT * kHD;                            // [2][64][128]
-  __nv_bfloat16* sq = sv + 2 * kKT * kHD;                            // [4 warps][16][128]
+  extern __shared__ __align__(1024) uint8_t smem_attn[];
+  constexpr int S = kStagesPF;
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_attn);  // [S][64][128]
+  __nv_bfloat16* sv = sk + S * kKT * kHD;                            // [S][64][128]
+  __nv_bfloat16* sq = sv + S * kKT * kHD;                            // [4 warps][16][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sq + 4 * 16 * kHD);
   const int2 wi = work[blockIdx.x];
   const AttnSeq sq_meta = seqs[wi.x];
   const int kvh = blockIdx.y;
@@ -235,10 +231,16 @@ __global__ void __launch_bounds__(kThreadsAttn)
   const int last_tok = min(sq_meta.q_len - 1, (wi.y + kRowsPF - 1) / g.group);
   const int kv_end = start + last_tok + 1;  // keys needed by this CTA
   const int n_tiles = (kv_end + kKT - 1) / kKT;
-
-  load_kv_tile(sk, kplane, pt, kv_end, 0, kvh, g);
-  load_kv_tile(sv, vplane, pt, kv_end, 0, kvh, g);
-  cp_async_commit();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  if (threadIdx.x == 0)
+    for (int t = 0; t < S && t < n_tiles; ++t)
+      issue_kv_tile(sk + t * kKT * kHD, sv + t * kKT * kHD, &full[t], kplane, vplane, pt, kv_end,
+                    t * kKT, kvh, g, pol);
 
   uint32_t qf[8][4];
   load_q_frag(qf, qkv, g, sq_meta.q_start, sq_meta.q_len, row0, kvh, sq + warp * 16 * kHD);
@@ -256,19 +258,14 @@ __global__ void __launch_bounds__(kThreadsAttn)
     for (int i = 0; i < 4; ++i) o[d][i] = 0.f;
 
   for (int t = 0; t < n_tiles; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < n_tiles) {
-      load_kv_tile(sk + (buf ^ 1) * kKT * kHD, kplane, pt, kv_end, (t + 1) * kKT, kvh, g);
-      load_kv_tile(sv + (buf ^ 1) * kKT * kHD, vplane, pt, kv_end, (t + 1) * kKT, kvh, g);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    const int buf = t % S;
+    mbar_wait(&full[buf], (t / S) & 1);
     attend_tile<true>(qf, sk + buf * kKT * kHD, sv + buf * kKT * kHD, 0, kKT, row_limit, m, l, o,
                       g.scale_log2, t * kKT);
-    __syncthreads();
+    __syncthreads();  // every warp is done with buf
+    if (threadIdx.x == 0 && t + S < n_tiles)
+      issue_kv_tile(sk + buf * kKT * kHD, sv + buf * kKT * kHD, &full[buf], kplane, vplane, pt,
+                    kv_end, (t + S) * kKT, kvh, g, pol);
   }
   // normalize + store
 #pragma unroll
@@ -302,11 +299,13 @@ __global__ void __launch_bounds__(kThreadsAttn)
                        const int32_t* __restrict__ pages, int splits, int tiles_per_split,
                        __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
                        float* __restrict__ part_ml) {
-  extern __shared__ __align__(128) uint8_t smem_attn[];
+  extern __shared__ __align__(1024) uint8_t smem_attn[];
+  constexpr int S = kStagesDec;
   __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_attn);
-  __nv_bfloat16* sv = sk + 2 * kKT * kHD;
-  __nv_bfloat16* sq = sv + 2 * kKT * kHD;  // 16 x 128
+  __nv_bfloat16* sv = sk + S * kKT * kHD;
+  __nv_bfloat16* sq = sv + S * kKT * kHD;  // 16 x 128
   float* red = reinterpret_cast<float*>(sq + 16 * kHD);  // merge scratch
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 128 + 16 * kHD);
   const int seq = blockIdx.x / splits, split = blockIdx.x % splits;
   const int kvh = blockIdx.y;
   const AttnSeq meta = seqs[seq];
@@ -315,6 +314,16 @@ __global__ void __launch_bounds__(kThreadsAttn)
   const int total_tiles = (meta.kv_len + kKT - 1) / kKT;
   const int t0 = split * tiles_per_split;
   const int t1 = min(total_tiles, t0 + tiles_per_split);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  if (threadIdx.x == 0)
+    for (int t = t0; t < t1 && t < t0 + S; ++t)
+      issue_kv_tile(sk + (t - t0) * kKT * kHD, sv + (t - t0) * kKT * kHD, &full[t - t0], kplane,
+                    vplane, pt, meta.kv_len, t * kKT, kvh, g, pol);
 
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
   float o[16][4];
@@ -322,12 +331,6 @@ __global__ void __launch_bounds__(kThreadsAttn)
   for (int d = 0; d < 16; ++d)
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[d][i] = 0.f;
-
-  if (t0 < t1) {
-    load_kv_tile(sk, kplane, pt, meta.kv_len, t0 * kKT, kvh, g);
-    load_kv_tile(sv, vplane, pt, meta.kv_len, t0 * kKT, kvh, g);
-    cp_async_commit();
-  }
   uint32_t qf[8][4];
   // every warp loads the same 16-row Q fragment (rows >= G are zero)
   {
@@ -347,22 +350,17 @@ __global__ void __launch_bounds__(kThreadsAttn)
       ldsm_x4(qf[k], sq + swz(row, col));
     }
   }
+  const int lim[2] = {meta.kv_len - 1, meta.kv_len - 1};
   for (int t = t0; t < t1; ++t) {
-    const int buf = (t - t0) & 1;
-    if (t + 1 < t1) {
-      load_kv_tile(sk + (buf ^ 1) * kKT * kHD, kplane, pt, meta.kv_len, (t + 1) * kKT, kvh, g);
-      load_kv_tile(sv + (buf ^ 1) * kKT * kHD, vplane, pt, meta.kv_len, (t + 1) * kKT, kvh, g);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    const int i = t - t0, buf = i % S;
+    mbar_wait(&full[buf], (i / S) & 1);
     // this warp's 16-key slice; keys past kv_len are masked via the limit
-    const int lim[2] = {meta.kv_len - 1, meta.kv_len - 1};
     attend_tile<true>(qf, sk + buf * kKT * kHD, sv + buf * kKT * kHD, warp * 16, warp * 16 + 16,
                       lim, m, l, o, g.scale_log2, t * kKT);
     __syncthreads();
+    if (threadIdx.x == 0 && t + S < t1)
+      issue_kv_tile(sk + buf * kKT * kHD, sv + buf * kKT * kHD, &full[buf], kplane, vplane, pt,
+                    meta.kv_len, (t + S) * kKT, kvh, g, pol);
   }
   // merge the 4 warps: rows 0..G-1 live in lanes 0..(4*G-1) (row = lane/4).
 #pragma unroll
@@ -444,9 +442,13 @@ __global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ se
 
 }  // namespace
 
-size_t attn_smem_bytes() {
-  return static_cast<size_t>(4 * kKT * kHD + 4 * 16 * kHD) * 2 + (128 + 16 * kHD) * 4 + 64;
+size_t attn_smem_bytes_pf() {
+  return static_cast<size_t>(2 * kStagesPF * kKT * kHD + 4 * 16 * kHD) * 2 + 64;
 }
+size_t attn_smem_bytes_dec() {
+  return static_cast<size_t>(2 * kStagesDec * kKT * kHD + 16 * kHD) * 2 + (128 + 16 * kHD) * 4 + 64;
+}
+size_t attn_smem_bytes() { return std::max(attn_smem_bytes_pf(), attn_smem_bytes_dec()); }
 
 cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                               const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
@@ -454,11 +456,9 @@ cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                               const int32_t* pages, __nv_bfloat16* out, cudaStream_t s) {
   if (n_work == 0) return cudaSuccess;
   static bool configured = false;
-  const size_t smem = attn_smem_bytes();
+  const size_t smem = attn_smem_bytes_pf();
   if (!configured) {
     cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     configured = true;
   }
@@ -474,11 +474,9 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              __nv_bfloat16* out, float* part_o, float* part_ml, size_t part_cap,
                              int sm_count, cudaStream_t s) {
   if (n_seq == 0) return cudaSuccess;
-  const size_t smem = attn_smem_bytes();
+  const size_t smem = attn_smem_bytes_dec();
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
     cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     configured = true;

@@ -97,13 +97,19 @@ cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int 
 // out[r] = x[rows ? rows[r] : r] * rsqrt(mean(x^2) + eps) * w
 cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows, int n, int hidden,
                     const __nv_bfloat16* w, float eps, __nv_bfloat16* out, cudaStream_t s);
-// Rotary embedding on q and k (rotate-half pairs), then k, v -> paged cache.
-cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* pos,
-                          const int32_t* slot, const float* inv_freq, int n_heads, int n_kv_heads,
-                          int head_dim, int page_tokens, __nv_bfloat16* kplane,
-                          __nv_bfloat16* vplane, cudaStream_t s);
-// out[r] = argmax_j logits[r, j] (lowest index on ties)
-cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, cudaStream_t s);
+// Per-batch RoPE cos/sin table [n_tokens][head_dim / 2].
+cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, int head_dim,
+                       float2* table, cudaStream_t s);
+// Rotary embedding on q and k (rotate-half pairs), then k, v -> paged cache
+// in the pre-swizzled page layout the attention kernels bulk-copy.
+cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* slot,
+                          const float2* table, int n_heads, int n_kv_heads, int head_dim,
+                          int page_tokens, __nv_bfloat16* kplane, __nv_bfloat16* vplane,
+                          cudaStream_t s);
+// out[r] = argmax_j logits[r, j] (lowest index on ties); scratch holds
+// 16 float2 per row.
+cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, float2* scratch,
+                        cudaStream_t s);
 // Deterministic random bf16 fill: uniform(-scale, scale) + offset from a hash of (seed, i).
 cudaError_t fill_random(__nv_bfloat16* p, size_t n, uint64_t seed, float scale, float offset,
                         cudaStream_t s);

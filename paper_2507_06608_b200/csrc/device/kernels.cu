@@ -67,74 +67,97 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_
   }
 }
 
-// grid = tokens; block = (H + Hkv) * hd/2 / 8 threads... simple: loop.
-// q/k heads rotate pairs (i, i + hd/2) by angle pos * inv_freq[i].
-__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
-                               const int32_t* __restrict__ slot, const float* __restrict__ inv_freq,
-                               int n_heads, int n_kv_heads, int hd, int page_tokens,
-                               __nv_bfloat16* __restrict__ kplane, __nv_bfloat16* __restrict__ vplane) {
+// cos/sin of pos * inv_freq[j] for every token of the batch, computed once
+// per forward and shared by all layers: table[t][j] = (cos, sin).
+__global__ void rope_table_kernel(const int32_t* __restrict__ pos, const float* __restrict__ inv_freq,
+                                  int half, float2* __restrict__ table) {
   const int t = blockIdx.x;
-  const int stride = (n_heads + 2 * n_kv_heads) * hd;
-  __nv_bfloat16* row = qkv + static_cast<size_t>(t) * stride;
   const float p = static_cast<float>(pos[t]);
-  const int half = hd / 2;
-  const int s = slot[t];
-  const int page = s / page_tokens, off = s % page_tokens;
-  // rotation of q and k heads: (n_heads + n_kv_heads) * half pairs
-  const int pairs = (n_heads + n_kv_heads) * half;
-  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
-    const int head = i / half, j = i % half;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
     float sn, cs;
     sincosf(p * inv_freq[j], &sn, &cs);
-    __nv_bfloat16* h = row + head * hd;
-    const float a = __bfloat162float(h[j]), b = __bfloat162float(h[j + half]);
-    const __nv_bfloat16 ra = __float2bfloat16(a * cs - b * sn);
-    const __nv_bfloat16 rb = __float2bfloat16(b * cs + a * sn);
-    if (head < n_heads) {
-      h[j] = ra;
-      h[j + half] = rb;
-    } else {
-      const int kh = head - n_heads;
-      __nv_bfloat16* dst =
-          kplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * page_tokens + off) * hd;
-      dst[j] = ra;
-      dst[j + half] = rb;
-      h[j] = ra;
-      h[j + half] = rb;
-    }
-  }
-  // v heads copy (16 B vectors)
-  const int vvec = n_kv_heads * hd / 8;
-  const __nv_bfloat16* vsrc = row + (n_heads + n_kv_heads) * hd;
-  for (int i = threadIdx.x; i < vvec; i += blockDim.x) {
-    const int kh = (i * 8) / hd, d = (i * 8) % hd;
-    __nv_bfloat16* dst =
-        vplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * page_tokens + off) * hd + d;
-    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(vsrc + i * 8);
+    table[static_cast<size_t>(t) * half + j] = make_float2(cs, sn);
   }
 }
 
-// One CTA per row; (value, index) reduction with lowest index on ties.
-__global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int32_t* __restrict__ out) {
-  const float* row = logits + static_cast<size_t>(blockIdx.x) * vocab;
+// One CTA per token. Work items: (q or k head, chunk pair p) rotates dims
+// [8p, 8p+8) with [64+8p, 64+8p+8) (rotate-half, hd = 128) using 16 B
+// vectors; q stays in the qkv buffer, k and v go to the paged cache in the
+// pre-swizzled layout (16 B chunk c of page row r at c ^ (r & 7)).
+__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ slot,
+                               const float2* __restrict__ table, int n_heads, int n_kv_heads,
+                               int page_tokens, __nv_bfloat16* __restrict__ kplane,
+                               __nv_bfloat16* __restrict__ vplane) {
+  constexpr int hd = 128, half = 64;
+  const int t = blockIdx.x;
+  const int stride = (n_heads + 2 * n_kv_heads) * hd;
+  __nv_bfloat16* row = qkv + static_cast<size_t>(t) * stride;
+  const int s = slot[t];
+  const int page = s / page_tokens, off = s % page_tokens;
+  const int sw = off & 7;
+  const float2* cs = table + static_cast<size_t>(t) * half;
+  const int rot_items = (n_heads + n_kv_heads) * 8;
+  const int v_items = n_kv_heads * 16;
+  for (int it = threadIdx.x; it < rot_items + v_items; it += blockDim.x) {
+    if (it < rot_items) {
+      const int head = it >> 3, p = it & 7;
+      __nv_bfloat16* h = row + head * hd;
+      const uint4 va = *reinterpret_cast<const uint4*>(h + 8 * p);
+      const uint4 vb = *reinterpret_cast<const uint4*>(h + half + 8 * p);
+      const __nv_bfloat16* a = reinterpret_cast<const __nv_bfloat16*>(&va);
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&vb);
+      __align__(16) __nv_bfloat16 ra[8], rb[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 c = cs[8 * p + i];
+        const float x = __bfloat162float(a[i]), y = __bfloat162float(b[i]);
+        ra[i] = __float2bfloat16(x * c.x - y * c.y);
+        rb[i] = __float2bfloat16(y * c.x + x * c.y);
+      }
+      if (head < n_heads) {
+        *reinterpret_cast<uint4*>(h + 8 * p) = *reinterpret_cast<uint4*>(ra);
+        *reinterpret_cast<uint4*>(h + half + 8 * p) = *reinterpret_cast<uint4*>(rb);
+      } else {
+        __nv_bfloat16* dst =
+            kplane + ((static_cast<size_t>(page) * n_kv_heads + (head - n_heads)) * page_tokens + off) * hd;
+        *reinterpret_cast<uint4*>(dst + ((p ^ sw) << 3)) = *reinterpret_cast<uint4*>(ra);
+        *reinterpret_cast<uint4*>(dst + (((p + 8) ^ sw) << 3)) = *reinterpret_cast<uint4*>(rb);
+      }
+    } else {
+      const int i = it - rot_items;
+      const int kh = i >> 4, c = i & 15;
+      const __nv_bfloat16* src = row + (n_heads + n_kv_heads + kh) * hd + c * 8;
+      __nv_bfloat16* dst =
+          vplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * page_tokens + off) * hd;
+      *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 3)) = *reinterpret_cast<const uint4*>(src);
+    }
+  }
+}
+
+// Greedy sampling, two passes: kArgChunks CTAs per row reduce a slice of
+// the vocabulary to one (value, index) pair; one warp per row folds them.
+// Ties resolve to the lowest index (numpy argmax).
+constexpr int kArgChunks = 16;
+
+__device__ __forceinline__ void arg_better(float& best, int& idx, float v, int i) {
+  if (v > best || (v == best && i < idx)) {
+    best = v;
+    idx = i;
+  }
+}
+
+__global__ void argmax_partial_kernel(const float* __restrict__ logits, int vocab,
+                                      float2* __restrict__ part) {
+  const int row = blockIdx.y, chunk = blockIdx.x;
+  const int per = (vocab + kArgChunks - 1) / kArgChunks;
+  const int lo = chunk * per, hi = min(vocab, lo + per);
+  const float* r = logits + static_cast<size_t>(row) * vocab;
   float best = -FLT_MAX;
   int idx = 0x7fffffff;
-  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-    const float v = row[i];
-    if (v > best || (v == best && i < idx)) {
-      best = v;
-      idx = i;
-    }
-  }
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) arg_better(best, idx, r[i], i);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffff, best, o);
-    const int oi = __shfl_xor_sync(0xffffffff, idx, o);
-    if (ov > best || (ov == best && oi < idx)) {
-      best = ov;
-      idx = oi;
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1)
+    arg_better(best, idx, __shfl_xor_sync(0xffffffff, best, o), __shfl_xor_sync(0xffffffff, idx, o));
   __shared__ float sv[32];
   __shared__ int si[32];
   if ((threadIdx.x & 31) == 0) {
@@ -143,13 +166,26 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int32
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
-      if (sv[w] > best || (sv[w] == best && si[w] < idx)) {
-        best = sv[w];
-        idx = si[w];
-      }
-    out[blockIdx.x] = idx;
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) arg_better(best, idx, sv[w], si[w]);
+    part[row * kArgChunks + chunk] = make_float2(best, __int_as_float(idx));
   }
+}
+
+__global__ void argmax_final_kernel(const float2* __restrict__ part, int rows, int32_t* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float best = -FLT_MAX;
+  int idx = 0x7fffffff;
+  if (lane < kArgChunks) {
+    const float2 p = part[row * kArgChunks + lane];
+    best = p.x;
+    idx = __float_as_int(p.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    arg_better(best, idx, __shfl_xor_sync(0xffffffff, best, o), __shfl_xor_sync(0xffffffff, idx, o));
+  if (lane == 0) out[row] = idx;
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -187,21 +223,32 @@ cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows, int n, int hidd
   return cudaGetLastError();
 }
 
-cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* pos,
-                          const int32_t* slot, const float* inv_freq, int n_heads, int n_kv_heads,
-                          int head_dim, int page_tokens, __nv_bfloat16* kplane,
-                          __nv_bfloat16* vplane, cudaStream_t s) {
+cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, int head_dim,
+                       float2* table, cudaStream_t s) {
   if (n_tokens == 0) return cudaSuccess;
   ++g_kernel_launches;
-  rope_kv_kernel<<<n_tokens, 256, 0, s>>>(qkv, pos, slot, inv_freq, n_heads, n_kv_heads, head_dim,
-                                          page_tokens, kplane, vplane);
+  rope_table_kernel<<<n_tokens, 64, 0, s>>>(pos, inv_freq, head_dim / 2, table);
   return cudaGetLastError();
 }
 
-cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
+cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* slot,
+                          const float2* table, int n_heads, int n_kv_heads, int head_dim,
+                          int page_tokens, __nv_bfloat16* kplane, __nv_bfloat16* vplane,
+                          cudaStream_t s) {
+  if (n_tokens == 0) return cudaSuccess;
+  if (head_dim != 128) return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  argmax_kernel<<<n, 1024, 0, s>>>(logits, vocab, out);
+  rope_kv_kernel<<<n_tokens, 128, 0, s>>>(qkv, slot, table, n_heads, n_kv_heads, page_tokens,
+                                          kplane, vplane);
+  return cudaGetLastError();
+}
+
+cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, float2* scratch,
+                        cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  g_kernel_launches += 2;
+  argmax_partial_kernel<<<dim3(kArgChunks, n), 256, 0, s>>>(logits, vocab, scratch);
+  argmax_final_kernel<<<(n + 7) / 8, 256, 0, s>>>(scratch, n, out);
   return cudaGetLastError();
 }
 

@@ -123,7 +123,8 @@ Model::Model(const nx_device_config& cfg) : cfg_(cfg), a_(cfg.arch) {
     throw std::invalid_argument("hidden/vocab must be multiples of 128, ffn of 64");
   if (a_.n_heads % a_.n_kv_heads || a_.n_heads / a_.n_kv_heads > 8)
     throw std::invalid_argument("GQA group must divide heads and be <= 8");
-  if (cfg.page_tokens < 1 || cfg.num_pages < 1) throw std::invalid_argument("bad page geometry");
+  if (cfg.page_tokens != 16 || cfg.num_pages < 1)
+    throw std::invalid_argument("page_tokens must be 16 (4 KB pre-swizzled KV runs)");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg.device)
     throw NoDevice("no CUDA device");
@@ -237,6 +238,7 @@ void LaneWs::init(Model* m, int max_tokens) {
   sample_cap = std::min<int>(t_max, 256);
   hs = static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(sample_cap) * a.hidden * 2));
   logits = static_cast<float*>(alloc(static_cast<size_t>(sample_cap) * a.vocab * 4));
+  rope_cs = static_cast<float2*>(alloc(T * (a.head_dim / 2) * sizeof(float2)));
   ws_bytes = 96u << 20;
   ws = static_cast<float*>(alloc(ws_bytes));
   ck(cudaMemset(ws, 0, gemm_counter_bytes()), "zero gemm counters");
@@ -419,6 +421,9 @@ void Model::forward(LaneWs& ws) {
   const double kvtok = 2.0 * a_.n_kv_heads * a_.head_dim * 2;  // K+V bytes per token per layer
   const double qo = 2.0 * attn_cols_ * 2;                       // q in + out per token
   timed(NX_K_OTHER, Td * d * 2 + Td * 4, 0, [&] { ck(embed(ws.d_tok, T, emb_, d, ws.x, s), "embed"); });
+  timed(NX_K_OTHER, Td * a_.head_dim * 4, 0, [&] {
+    ck(rope_table(ws.d_pos, T, inv_freq_, a_.head_dim, ws.rope_cs, s), "rope table");
+  });
   for (int l = 0; l < a_.n_layers; ++l) {
     const LayerW& w = layers_[l];
     __nv_bfloat16* kplane = kv_ + (2 * static_cast<size_t>(l)) * plane_elems_;
@@ -432,8 +437,8 @@ void Model::forward(LaneWs& ws) {
          "qkv gemm");
     });
     timed(NX_K_OTHER, Td * qkv_rows_ * 4, 0, [&] {
-      ck(rope_kv_write(ws.qkv, T, ws.d_pos, ws.d_slot, inv_freq_, a_.n_heads, a_.n_kv_heads,
-                       a_.head_dim, cfg_.page_tokens, kplane, vplane, s),
+      ck(rope_kv_write(ws.qkv, T, ws.d_slot, ws.rope_cs, a_.n_heads, a_.n_kv_heads, a_.head_dim,
+                       cfg_.page_tokens, kplane, vplane, s),
          "rope");
     });
     if (ws.dec_seq_count > 0)
@@ -486,7 +491,9 @@ void Model::forward(LaneWs& ws) {
                "lm_head gemm");
           });
     timed(NX_K_OTHER, nd * a_.vocab * 4, 0,
-          [&] { ck(argmax_rows(ws.logits, n, a_.vocab, ws.d_out_tokens + r0, s), "argmax"); });
+          [&] { ck(argmax_rows(ws.logits, n, a_.vocab, ws.d_out_tokens + r0,
+                            reinterpret_cast<float2*>(ws.part_ml), s),
+               "argmax"); });
   }
 }
 

@@ -50,6 +50,7 @@ struct LaneWs {
   __nv_bfloat16 *x = nullptr, *h = nullptr, *qkv = nullptr, *attn = nullptr, *act = nullptr,
                 *hs = nullptr;
   float* logits = nullptr;
+  float2* rope_cs = nullptr;  // per-batch RoPE table [t_max][64]
   int sample_cap = 0;
   float* ws = nullptr;
   size_t ws_bytes = 0;
