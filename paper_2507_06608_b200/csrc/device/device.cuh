@@ -38,6 +38,7 @@ struct GemmParams {
   int max_pieces;  // stream-K: partial slots per tile
   int bn;          // token tile (for the stream-K fix-up)
   int* tile_count; // stream-K: per-tile arrival counters (zero between launches)
+  int n_tiles128;  // 128-row weight blocks (n_mblk counts MT-block work tiles)
 };
 
 int gemm_pick_bn(int tokens);

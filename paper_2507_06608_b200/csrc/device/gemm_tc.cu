@@ -14,9 +14,9 @@
 //               into a double-buffered TMEM accumulator; owns TMEM alloc
 //   warps 2-5   epilogue: tcgen05.ld -> smem stage -> fused op -> coalesced
 //               16-byte global stores (bias / residual add / SwiGLU / fp32)
-// A work unit is (feature block, token block, K split). K splits > 1 write
-// fp32 partials that nxd_splitk_reduce() folds with the same epilogue; the
-// host picks splits so decode launches fill the lane's SM partition.
+// A work tile is MT (1-2) 128-row weight blocks x BN tokens. Decode shapes
+// use stream-K over (tile, k-block) iterations with an in-kernel fix-up;
+// forced K splits (tests) use a separate reduce kernel.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -36,14 +36,23 @@ constexpr int kThreads = 192;     // 6 warps
 constexpr int kEpiThreads = 128;
 constexpr int kABytes = kBM * kBK * 2;
 
-template <int BN>
+// A work tile is MT consecutive 128-row weight blocks x BN tokens: the MT
+// weight tiles of a stage share one activation tile, which cuts the shared-
+// memory traffic per weight byte (TMA write + MMA read of W, plus X) from
+// 3x to 2.5x at MT = 2 -- the per-SM bound of the decode (GEMV-like) shapes.
+constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+template <int BN, int MT>
 struct Cfg {
   static constexpr int kBBytes = BN * kBK * 2;
-  static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = BN >= 256 ? 4 : BN >= 128 ? 5 : BN >= 64 ? 8 : 9;
+  static constexpr int kStage = MT * kABytes + kBBytes;
   static constexpr int kEpiBytes = 32 * kBM * 4;
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int kBudget = 227 * 1024 - kEpiBytes - 1280;  // 227 KB opt-in smem per CTA
+  static constexpr int kStages = kBudget / kStage > 9 ? 9 : kBudget / kStage;
+  static constexpr int kTmemCols = pow2_cols(2 * MT * BN);
   static constexpr int kSmem = 1024 + kStages * kStage + kEpiBytes + 256;
+  static_assert(kStages >= 2, "pipeline too shallow");
+  static_assert(2 * MT * BN <= 512, "TMEM: 512 columns");
 };
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
@@ -160,7 +169,7 @@ struct WorkIter {
 // epilogue threads publish their fp32 partial, count the tile's arrivals
 // with one atomic, and the last CTA folds every piece of the tile and
 // applies the epilogue (classic threadfence reduction; no extra launch).
-template <int BN>
+template <int BN, int MT>
 __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& w, int et, int* s_flag) {
   const int tile = w.m_blk * p.n_nblk + w.n_blk;
   const long long total = static_cast<long long>(p.n_mblk) * p.n_nblk * p.num_kb;
@@ -180,14 +189,17 @@ __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& 
   __threadfence();
   const int tok_base = w.n_blk * BN;
   const int n_tok = min(BN, p.tokens - tok_base);
-  const float4* base =
-      reinterpret_cast<const float4*>(p.ws + static_cast<size_t>(tile) * p.max_pieces * BN * kBM);
-  constexpr int kSlot4 = BN * kBM / 4;  // float4 per piece slot
+  const float4* base = reinterpret_cast<const float4*>(
+      p.ws + static_cast<size_t>(tile) * p.max_pieces * MT * BN * kBM);
+  constexpr int kSlot4 = BN * kBM / 4;  // float4 per (piece, sub-tile) slot
+  const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
   // Each thread owns kPer float4 positions (coalesced: position = et + 128 i);
   // pieces are the outer loop so every pass issues kPer independent loads.
   constexpr int kPer = 8;
   const int n4 = n_tok * (kBM / 4);
+  for (int sub = 0; sub < valid; ++sub)
   for (int chunk = 0; chunk < n4; chunk += kEpiThreads * kPer) {
+    const int m128 = w.m_blk * MT + sub;
     float4 acc[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -196,7 +208,7 @@ __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& 
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         const int pos = chunk + et + i * kEpiThreads;
-        v[i] = pos < n4 ? __ldcg(base + q * kSlot4 + pos) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[i] = pos < n4 ? __ldcg(base + (q * MT + sub) * kSlot4 + pos) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
@@ -216,18 +228,18 @@ __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& 
         if (c >= 64) continue;  // gate half drives the output; up half read below
         float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int q = 0; q < pieces; ++q) {
-          const float4 b = __ldcg(base + q * kSlot4 + pos + 16);
+          const float4 b = __ldcg(base + (q * MT + sub) * kSlot4 + pos + 16);
           u.x += b.x, u.y += b.y, u.z += b.z, u.w += b.w;
         }
         __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo +
-                             w.m_blk * 64 + c;
+                             m128 * 64 + c;
         *reinterpret_cast<__nv_bfloat162*>(dst) =
             __floats2bfloat162_rn(silu(acc[i].x) * u.x, silu(acc[i].y) * u.y);
         *reinterpret_cast<__nv_bfloat162*>(dst + 2) =
             __floats2bfloat162_rn(silu(acc[i].z) * u.z, silu(acc[i].w) * u.w);
         continue;
       }
-      const int f = w.m_blk * kBM + c;
+      const int f = m128 * kBM + c;
       if (p.mode == kEpiF32) {
         *reinterpret_cast<float4*>(static_cast<float*>(p.out) + static_cast<size_t>(t) * p.ldo + f) =
             acc[i];
@@ -252,11 +264,11 @@ __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& 
   }
 }
 
-template <int BN>
+template <int BN, int MT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __nv_bfloat16* __restrict__ wpack, const __grid_constant__ CUtensorMap tx,
                    GemmParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -296,14 +308,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       WorkIter wi(p);
       Work w;
       while (wi.next(w)) {
+        const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStage;
-          mbar_expect_tx(&full[stage], C::kStage);
-          // weight tile = one contiguous 16 KB pre-swizzled chunk (see pack_weights)
-          bulk_load(sa, wpack + packed_tile_offset(w.m_blk, kb, p.num_kb), kABytes, &full[stage],
-                    w_policy);
-          tma_load_2d(&tx, &full[stage], sa + kABytes, kb * kBK, w.n_blk * BN);
+          mbar_expect_tx(&full[stage], valid * kABytes + C::kBBytes);
+          // weight tiles = contiguous pre-swizzled 16 KB chunks (pack_weights); an
+          // aligned pair of row blocks is one 32 KB copy
+          if (MT == 2 && valid == 2) {
+            bulk_load(sa, wpack + packed_tile_offset(w.m_blk * 2, kb, p.num_kb), 2 * kABytes,
+                      &full[stage], w_policy);
+          } else {
+            for (int t = 0; t < valid; ++t)
+              bulk_load(sa + t * kABytes, wpack + packed_tile_offset(w.m_blk * MT + t, kb, p.num_kb),
+                        kABytes, &full[stage], w_policy);
+          }
+          tma_load_2d(&tx, &full[stage], sa + MT * kABytes, kb * kBK, w.n_blk * BN);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -325,17 +345,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem + acc * BN;
+      const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t a_addr = smem_u32(smem + stage * C::kStage);
-          const uint32_t b_addr = a_addr + kABytes;
+          const uint32_t base = smem_u32(smem + stage * C::kStage);
+          const uint32_t b_addr = base + MT * kABytes;
+          for (int t = 0; t < valid; ++t) {
+            const uint32_t d = tmem + (acc * MT + t) * BN;
+            const uint32_t a_addr = base + t * kABytes;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            umma_bf16(d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
-                      idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma_bf16(d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                        idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
           umma_commit(&empty[stage]);
           if (kb == kb1 - 1) umma_commit(&tfull[acc]);
         }
@@ -359,12 +383,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int f0 = w.m_blk * kBM;
+      const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
+      for (int sub = 0; sub < valid; ++sub)
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int m128 = w.m_blk * MT + sub;
+        const int f0 = m128 * kBM;
         const int tok0 = w.n_blk * BN + c0;
         if (tok0 >= p.tokens) break;
         uint32_t r[32];
-        tmem_ld32(tmem + acc * BN + c0 + (static_cast<uint32_t>(q * 32) << 16), r);
+        tmem_ld32(tmem + (acc * MT + sub) * BN + c0 + (static_cast<uint32_t>(q * 32) << 16), r);
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) s_epi[j * kBM + q * 32 + lane] = __uint_as_float(r[j]);
@@ -379,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (t < p.tokens) {
               const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
               float* dst = p.streamk
-                               ? p.ws + (static_cast<size_t>(w.slot) * BN + c0 + j) * kBM + g * 4
+                               ? p.ws + ((static_cast<size_t>(w.slot) * MT + sub) * BN + c0 + j) * kBM + g * 4
                                : p.ws + (static_cast<size_t>(w.slot) * p.tokens + t) * p.rows + f0 + g * 4;
               *reinterpret_cast<float4*>(dst) = v;
             }
@@ -400,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 o[i] = __float2bfloat16(silu(gt) * up);
               }
               __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) +
-                                   static_cast<size_t>(t) * p.ldo + w.m_blk * 64 + g * 8;
+                                   static_cast<size_t>(t) * p.ldo + m128 * 64 + g * 8;
               *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(o);
             }
           }
@@ -453,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (p.streamk && w.partial) streamk_arrive<BN>(p, w, et, s_flag);
+      if (p.streamk && w.partial) streamk_arrive<BN, MT>(p, w, et, s_flag);
     }
   }
   __syncthreads();
@@ -516,19 +543,19 @@ __global__ void splitk_reduce_kernel(GemmParams p, int final_mode) {
       *reinterpret_cast<uint4*>(o);
 }
 
-template <int BN>
+template <int BN, int MT>
 cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const GemmParams& p, int grid,
                       cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, MT>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, MT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   ++g_kernel_launches;
-  gemm_tc_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(tw, tx, p);
+  gemm_tc_kernel<BN, MT><<<grid, kThreads, C::kSmem, s>>>(tw, tx, p);
   return cudaGetLastError();
 }
 
@@ -570,7 +597,13 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
   p.rows = rows;
   p.tokens = tokens;
   p.K = K;
-  p.n_mblk = rows / kBM;
+  // Two weight blocks per work tile only pay off on small partitions, where
+  // per-SM shared-memory traffic is the bound (gate_up on 16 SMs: +39%); at
+  // full occupancy the stream-K fix-up of 2-block tiles serializes (ncu:
+  // per-SM active cycles 70K..184K), so larger partitions keep MT = 1.
+  const int mt = (bn <= 64 && sm_count <= 24) ? 2 : 1;
+  p.n_tiles128 = rows / kBM;
+  p.n_mblk = (p.n_tiles128 + mt - 1) / mt;
   p.n_nblk = (tokens + bn - 1) / bn;
   p.num_kb = K / kBK;
   p.mode = mode;
@@ -596,6 +629,13 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
     p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
     if (static_cast<size_t>(p.splits) * tokens * rows * 4 > ws_bytes) return cudaErrorInvalidValue;
     grid = std::max(1, std::min(tiles * p.splits, sm_count));
+  } else if (mt == 2 && ws != nullptr && tiles < sm_count) {
+    // small partition: K splits until every SM has a unit (balanced, no fix-up)
+    int splits = std::min((sm_count + tiles - 1) / tiles, std::max(1, p.num_kb / 8));
+    while (splits > 1 && static_cast<size_t>(splits) * tokens * rows * 4 > ws_bytes) --splits;
+    p.kb_per_split = (p.num_kb + splits - 1) / splits;
+    p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+    grid = std::max(1, std::min(tiles * p.splits, sm_count));
   } else if (tokens <= 256 && ws != nullptr && tiles % sm_count != 0 &&
              static_cast<size_t>(tiles) * 4 <= gemm_counter_bytes()) {
     // Stream-K: equal (tile, k-block) ranges per CTA remove the wave tail
@@ -603,7 +643,7 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
     const int G = static_cast<int>(std::min<long long>(sm_count, iters));
     const long long per_min = iters / G;
     p.max_pieces = static_cast<int>((p.num_kb + per_min - 1) / per_min) + 1;
-    const size_t need = static_cast<size_t>(tiles) * p.max_pieces * bn * kBM * 4;
+    const size_t need = static_cast<size_t>(tiles) * p.max_pieces * mt * bn * kBM * 4;
     if (need <= ws_bytes && tiles < 8 * G) {
       p.streamk = 1;
       grid = G;
@@ -614,11 +654,13 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
     grid = std::max(1, std::min(tiles, sm_count));
   }
   cudaError_t e;
-  switch (bn) {
-    case 32: e = launch_bn<32>(w_map, x_map_for_bn, p, grid, stream); break;
-    case 64: e = launch_bn<64>(w_map, x_map_for_bn, p, grid, stream); break;
-    case 128: e = launch_bn<128>(w_map, x_map_for_bn, p, grid, stream); break;
-    case 256: e = launch_bn<256>(w_map, x_map_for_bn, p, grid, stream); break;
+  switch (bn * 4 + mt) {
+    case 32 * 4 + 1: e = launch_bn<32, 1>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 32 * 4 + 2: e = launch_bn<32, 2>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 64 * 4 + 1: e = launch_bn<64, 1>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 64 * 4 + 2: e = launch_bn<64, 2>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 128 * 4 + 1: e = launch_bn<128, 1>(w_map, x_map_for_bn, p, grid, stream); break;
+    case 256 * 4 + 1: e = launch_bn<256, 1>(w_map, x_map_for_bn, p, grid, stream); break;
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
