@@ -39,10 +39,18 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-# Reference ModelConfig preset "8b" (presets.cpp:16) drives the cost model;
-# the kernel view is Llama-3.1-8B (GQA 32/8, SwiGLU 14336, vocab 128256).
-REF_KVBPT_8B = 2 * 32 * 4096 * 2       # reference formula, bytes/token
-REAL_KVBPT_8B = 2 * 32 * 8 * 128 * 2   # real GQA bytes/token
+# model -> (reference ModelConfig dims for the cost model (presets.cpp:13-19;
+# 70B is derived the same way), real KV bytes/token of the kernel view).
+MODELS = {
+    "llama3-8b": ((4096, 14336, 32, 32, 2), 2 * 32 * 8 * 128 * 2),
+    "qwen2.5-14b": ((5120, 13824, 48, 40, 2), 2 * 48 * 8 * 128 * 2),
+    "llama3-70b": ((8192, 28672, 80, 64, 2), 2 * 80 * 8 * 128 * 2),
+}
+
+
+def ref_kvbpt(model: str) -> int:
+    d, _, L, _, e = MODELS[model][0]
+    return 2 * L * d * e
 
 
 def parse():
@@ -54,14 +62,16 @@ def parse():
     p.add_argument("--engine", default="nexus", choices=["nexus", "static", "monolithic"])
     p.add_argument("--rate", type=float, default=128.0)
     p.add_argument("--requests", type=int, default=480)
-    p.add_argument("--model", default="llama3-8b")
+    p.add_argument("--model", default="llama3-8b", choices=sorted(MODELS))
+    p.add_argument("--workload", default="sharegpt",
+                   help="trace preset: sharegpt | mixed | long-data | arxiv | longbench | bursty")
     p.add_argument("--kv-gb", type=float, default=80.0)
     p.add_argument("--slo-ttft", type=float, default=1.0)
     p.add_argument("--slo-tbt", type=float, default=0.05)
     p.add_argument("--profile-every", type=int, default=8)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-green", action="store_true")
-    p.add_argument("--calib", default=os.path.join(REPO, "profiles", "b200_llama3_8b"),
+    p.add_argument("--calib", default=None,
                    help="calibration base path (.calib + .json from paper_2507_06608_b200.calibrate); "
                         "'none' = reference default profile and nominal B200 spec")
     p.add_argument("--no-bw-ext", action="store_true", help="disable the share-dependent bandwidth term")
@@ -188,13 +198,13 @@ def load_calib(base):
 
 
 def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True, max_decode_batch=64,
-             alpha=1.3, beta=1.1):
-    m = nx.model_preset("8b")
+             alpha=1.3, beta=1.1, model="llama3-8b"):
+    m = nx.derive(*MODELS[model][0])
     slack = 4096
     cap_tokens = (num_pages - slack) * page_tokens
     cal = load_calib(calib)
     C, B, prof, bw_sat = (1.6595e15, 6.5562e12, None, None) if cal is None else cal
-    g = nx.gpu_spec(148, C, B, cap_tokens * REF_KVBPT_8B)
+    g = nx.gpu_spec(148, C, B, cap_tokens * ref_kvbpt(model))
     kind = {"nexus": nx.NX_ENGINE_NEXUS, "static": nx.NX_ENGINE_STATIC,
             "monolithic": nx.NX_ENGINE_MONOLITHIC}[engine]
     ctrl = nx.lib().nx_controller_config_default()
@@ -214,13 +224,13 @@ def run_reference(args, rank, world, dist):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libnexussim_ref.so not built"}))
         return
     page_tokens = 16
-    num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * REAL_KVBPT_8B))
+    num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * MODELS[args.model][1]))
     cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext, args.max_decode_batch,
-                   args.alpha, args.beta)
+                   args.alpha, args.beta, args.model)
     good = span = window = out = wall = 0.0
     ttft, tbt, decisions = [], [], 0
     for step in range(args.warmup + args.steps):
-        trace = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed + step)
+        trace = nx.workload_trace(args.workload, args.rate, args.requests, args.seed + step)
         t0 = time.perf_counter()
         r = reference.run(cfg, trace)
         t1 = time.perf_counter()
@@ -242,7 +252,8 @@ def run_reference(args, rank, world, dist):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "Llama-3.1-8B (reference 8b preset), sharegpt Poisson", "rate_rps": args.rate,
+        "config": {"workload": f"{args.model} (reference cost-model preset), {args.workload} trace",
+                   "rate_rps": args.rate,
                    "requests_per_step": args.requests, "engine": args.engine,
                    "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt}},
         "ttft_p50": nearest_rank(ttft, 50), "ttft_p99": nearest_rank(ttft, 99),
@@ -257,6 +268,8 @@ def run_reference(args, rank, world, dist):
 
 def main():
     args = parse()
+    if args.calib is None:
+        args.calib = os.path.join(REPO, "profiles", "b200_" + args.model.replace(".", "_").replace("-", "_"))
     rank, world, local, dist = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, rank, world, dist)
@@ -266,19 +279,19 @@ def main():
     from paper_2507_06608_b200 import device as D
 
     page_tokens = 16
-    num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * REAL_KVBPT_8B))
+    num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * MODELS[args.model][1]))
     dev = D.Device(D.arch_preset(args.model), num_pages=num_pages, page_tokens=page_tokens,
                    max_prefill_tokens=2048 + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
                    green_contexts=not args.no_green,
                    seed=args.seed, device=local)
     dev.set_profiling(args.profile_every)
     cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext, args.max_decode_batch,
-                   args.alpha, args.beta)
+                   args.alpha, args.beta, args.model)
     vocab = dev.arch.vocab
     rng = np.random.default_rng(args.seed + 7919 * rank)
 
     def one_step(step):
-        trace = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed + step + 1000 * rank)
+        trace = nx.workload_trace(args.workload, args.rate, args.requests, args.seed + step + 1000 * rank)
         prompts = [rng.integers(0, vocab, t.prompt_len, dtype=np.int32) for t in trace]
         t0 = time.perf_counter()
         eng = nx.Engine(cfg, device=dev)
@@ -363,9 +376,9 @@ def main():
     try:
         from oracle import reference
         if reference.available():
-            tr = nx.workload_trace("sharegpt", args.rate, args.requests, args.seed)
+            tr = nx.workload_trace(args.workload, args.rate, args.requests, args.seed)
             vcfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext, args.max_decode_batch,
-                   args.alpha, args.beta)
+                   args.alpha, args.beta, args.model)
             t0 = time.perf_counter()
             rr = reference.run(vcfg, tr)
             cw = time.perf_counter() - t0
@@ -381,7 +394,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall_max / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, sharegpt-shaped lengths, random prompt ids)",
-        "config": {"workload": "Llama-3.1-8B bf16, 1 B200 per rank, sharegpt Poisson (BASELINE configs[1])",
+        "config": {"workload": f"{args.model} bf16, 1 B200 per rank, {args.workload} trace"
+                               + (" (BASELINE configs[1])" if args.model == "llama3-8b" and args.workload == "sharegpt" else ""),
                    "rate_rps": args.rate, "requests_per_step": args.requests, "engine": args.engine,
                    "clock": "device", "green_contexts": not args.no_green,
                    "calibration": os.path.basename(args.calib) if load_calib(args.calib) else "none",

@@ -316,7 +316,9 @@ int nx_chunked_mixed_schedule(const nx_prefill_entry* queue, size_t n_queue,
 
 /* ---- traces (reference: workload.hpp:20-81, presets.hpp:28-43) ----------- */
 /* generate_trace/mix_traces via workload_preset + realize (presets.cpp:70-105).
- * preset: "long-data" | "arxiv" | "sharegpt" | "mixed". Writes min(count, cap). */
+ * preset: "long-data" | "arxiv" | "sharegpt" | "mixed" (reference) or, new,
+ * "longbench" (uniform 4096..16384-token prompts, ShareGPT outputs) and
+ * "bursty" ("mixed" lengths, Gamma inter-arrivals with CV 4). Writes min(count, cap). */
 int nx_workload_preset_trace(const char* preset, double rate_rps, int64_t count, uint64_t seed,
                              nx_request* out, size_t cap, size_t* n_out);
 /* Trace file text "# nexustrace v1" (workload.cpp:200-243). */

@@ -39,6 +39,21 @@ class Stream {
     const double u2 = uniform();
     return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
   }
+  // Gamma(shape, 1): Marsaglia-Tsang for shape >= 1, boosted for shape < 1.
+  double gamma(double shape) {
+    if (shape < 1.0) return gamma(shape + 1.0) * std::pow(uniform(), 1.0 / shape);
+    const double d = shape - 1.0 / 3.0, c = 1.0 / std::sqrt(9.0 * d);
+    for (;;) {
+      double x, v;
+      do {
+        x = gaussian();
+        v = 1.0 + c * x;
+      } while (v <= 0.0);
+      v = v * v * v;
+      const double u = uniform();
+      if (std::log(u) < 0.5 * x * x + d - d * v + d * std::log(v)) return d * v;
+    }
+  }
 
  private:
   std::mt19937_64 g_;
@@ -120,6 +135,39 @@ std::vector<nx_request> mixture(const std::vector<Component>& cs, const std::vec
   return out;
 }
 
+// New shapes (not in the reference presets): LongBench-shaped long prompts
+// (uniform 4096..16384 tokens, ShareGPT-shaped outputs) and
+// bursty arrivals (Gamma inter-arrival times with CV = 4, i.e. shape 1/16,
+// over the "mixed" length mix; C4).
+std::vector<nx_request> longbench(double rate, int64_t count, uint64_t seed) {
+  Stream arr(seed, kArrivals), len(seed, kLengths);
+  const Lengths out = sharegpt().out;
+  std::vector<nx_request> v;
+  double t = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    t += arr.exponential(rate);
+    nx_request r{};
+    r.id = static_cast<uint64_t>(i);
+    r.arrival_s = t;
+    r.prompt_len = 4096 + static_cast<int64_t>(len.uniform() * (16384 - 4096 + 1));
+    r.output_len = out.draw(len);
+    v.push_back(r);
+  }
+  return v;
+}
+
+std::vector<nx_request> bursty(double rate, int64_t count, uint64_t seed, double cv) {
+  std::vector<nx_request> v = mixture({sharegpt(), long_data()}, {0.6, 0.4}, rate, count, seed);
+  Stream arr(seed, 7);  // separate stream: lengths stay those of "mixed"
+  const double shape = 1.0 / (cv * cv), scale = 1.0 / (rate * shape);
+  double t = 0;
+  for (nx_request& r : v) {
+    t += arr.gamma(shape) * scale;
+    r.arrival_s = t;
+  }
+  return v;
+}
+
 }  // namespace
 
 std::vector<nx_request> preset_trace(const std::string& preset, double rate, int64_t count,
@@ -130,6 +178,8 @@ std::vector<nx_request> preset_trace(const std::string& preset, double rate, int
   if (preset == "long-data") return single(long_data(), rate, count, seed);
   if (preset == "arxiv") return single(arxiv(), rate, count, seed);
   if (preset == "mixed") return mixture({sharegpt(), long_data()}, {0.6, 0.4}, rate, count, seed);
+  if (preset == "longbench") return longbench(rate, count, seed);
+  if (preset == "bursty") return bursty(rate, count, seed, 4.0);
   throw InvalidArg("unknown workload preset '" + preset + "'");
 }
 

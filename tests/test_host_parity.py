@@ -326,3 +326,28 @@ def test_cost_ext_disabled_is_reference_and_port_mirrors_enabled(nx, ref):
     finally:
         nx.set_cost_ext(None)
     assert slow > 2.5 * base
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_engine_logs_match_committed_golden(nx, name):
+    """Same check without the reference library: committed sha256 fingerprints
+    of the reference's logs (tests/golden/make_golden.py)."""
+    import json
+    import os
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))[name]
+    fx, _ = _fixtures(nx)
+    model, gpu, kw, (preset, rate, count, seed) = fx[name]
+    trace = nx.workload_trace(preset, rate, count, seed)
+    assert hashlib.sha256(nx.trace_text(trace).encode()).hexdigest() == golden["trace_sha256"]
+    r = nx.run(nx.sim_config(model, gpu, **kw), trace)
+    assert hashlib.sha256(r.event_log.encode()).hexdigest() == golden["event_log_sha256"]
+    assert hashlib.sha256(r.decision_log.encode()).hexdigest() == golden["decision_log_sha256"]
+    assert hashlib.sha256(r.summary_json.encode()).hexdigest() == golden["summary_sha256"]
+    assert r.timed_out == golden["timed_out"] and r.sim_end_s == golden["sim_end_s"]
+
+
+def test_c1_trace_file_golden(nx):
+    import os
+    text = open(os.path.join(os.path.dirname(__file__), "golden", "c1_mixed_64_2.5rps_seed1.trace")).read()
+    assert nx.trace_text(nx.workload_trace("mixed", 2.5, 64, 1)) == text
+    assert nx.trace_text(nx.parse_trace(text)) == text
