@@ -79,6 +79,8 @@ def parse():
                    help="ControllerConfig.beta, the decode slack in prefill-prioritized mode. The paper's "
                         "1.1 was set for L20; on B200 a 2.0x slack still keeps p99 TBT well inside the "
                         "50 ms SLO (profiles/r01_beta_sweep.md)")
+    p.add_argument("--gamma", type=float, default=15.0,
+                   help="ControllerConfig.gamma (SPF aging, tokens of priority per second waited; reference 15)")
     p.add_argument("--alpha", type=float, default=1.3, help="ControllerConfig.alpha (prefill slack, paper 1.3)")
     p.add_argument("--max-decode-batch", type=int, default=128,
                    help="ControllerConfig.max_decode_batch (reference default 64, domain.hpp:87)")
@@ -198,7 +200,7 @@ def load_calib(base):
 
 
 def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True, max_decode_batch=64,
-             alpha=1.3, beta=1.1, model="llama3-8b"):
+             alpha=1.3, beta=1.1, model="llama3-8b", gamma=None):
     m = nx.derive(*MODELS[model][0])
     slack = 4096
     cap_tokens = (num_pages - slack) * page_tokens
@@ -210,6 +212,8 @@ def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True,
     ctrl = nx.lib().nx_controller_config_default()
     ctrl.max_decode_batch = max_decode_batch
     ctrl.alpha, ctrl.beta = alpha, beta
+    if gamma is not None:
+        ctrl.gamma = gamma
     return nx.sim_config(m, g, kind=kind, clock_mode=clock_mode, profile=prof, ctrl=ctrl,
                          bw_sat=bw_sat if bw_ext else None)
 
@@ -226,7 +230,7 @@ def run_reference(args, rank, world, dist):
     page_tokens = 16
     num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * MODELS[args.model][1]))
     cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext, args.max_decode_batch,
-                   args.alpha, args.beta, args.model)
+                   args.alpha, args.beta, args.model, args.gamma)
     good = span = window = out = wall = 0.0
     ttft, tbt, decisions = [], [], 0
     for step in range(args.warmup + args.steps):
@@ -286,7 +290,7 @@ def main():
                    seed=args.seed, device=local)
     dev.set_profiling(args.profile_every)
     cfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext, args.max_decode_batch,
-                   args.alpha, args.beta, args.model)
+                   args.alpha, args.beta, args.model, args.gamma)
     vocab = dev.arch.vocab
     rng = np.random.default_rng(args.seed + 7919 * rank)
 
@@ -378,7 +382,7 @@ def main():
         if reference.available():
             tr = nx.workload_trace(args.workload, args.rate, args.requests, args.seed)
             vcfg = make_cfg(nx, args.engine, num_pages, page_tokens, nx.NX_CLOCK_VIRTUAL, args.calib, not args.no_bw_ext, args.max_decode_batch,
-                   args.alpha, args.beta, args.model)
+                   args.alpha, args.beta, args.model, args.gamma)
             t0 = time.perf_counter()
             rr = reference.run(vcfg, tr)
             cw = time.perf_counter() - t0
@@ -401,7 +405,7 @@ def main():
                    "calibration": os.path.basename(args.calib) if load_calib(args.calib) else "none",
                    "bw_ext": not args.no_bw_ext,
                    "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt},
-                   "max_decode_batch": args.max_decode_batch, "alpha": args.alpha, "beta": args.beta,
+                   "max_decode_batch": args.max_decode_batch, "alpha": args.alpha, "beta": args.beta, "gamma": args.gamma,
                    "kv_pool_gb": args.kv_gb, "parallelism": f"replicas x{world}",
                    "l2": "inputs > L2 (16 GB weights streamed per decode step)"},
         "ttft_p50": nearest_rank(ttft, 50), "ttft_p99": nearest_rank(ttft, 99),

@@ -461,6 +461,28 @@ typedef struct nx_arch {
   float rms_eps;
 } nx_arch;
 
+/* Tensor-parallel shard of one rank: QKV / gate-up
+ * column-parallel, O / down row-parallel + all-reduce, vocab-parallel lm_head. */
+typedef struct nx_tp_shard {
+  int32_t tp_size, rank;
+  int32_t q_head0, n_q_heads;
+  int32_t kv_head0, n_kv_heads;
+  int32_t ffn0, ffn_local;
+  int32_t vocab0, vocab_local, vocab_valid, vocab_padded;
+} nx_tp_shard;
+int nx_tp_shard_plan(const nx_arch* arch, int32_t tp_size, int32_t rank, nx_tp_shard* out);
+/* NCCL unique id (128 bytes) for a communicator; rank 0 creates, the caller
+ * distributes (e.g. torch.distributed), every rank passes it to nx_device_create. */
+int nx_nccl_unique_id(uint8_t out[128]);
+
+/* Tensor-parallel execution modes.
+ * NX_TP_NCCL: one process per GPU; this nx_device is rank tp_rank and talks
+ *   to its peers through NCCL (all engines must issue identical batches).
+ * NX_TP_PEER: this nx_device drives all tp_size ranks itself, rank r on CUDA
+ *   device (device + r), collectives are peer-memory kernels over NVLink.
+ * NX_TP_PEER_COLOCATED: as NX_TP_PEER with every rank on `device` (tests). */
+enum { NX_TP_NCCL = 0, NX_TP_PEER = 1, NX_TP_PEER_COLOCATED = 2 };
+
 typedef struct nx_device_config {
   nx_arch arch;
   int32_t device;             /* CUDA ordinal */
@@ -472,6 +494,11 @@ typedef struct nx_device_config {
   uint64_t weight_seed;
   float weight_gain;   /* weights ~ U(+-gain * sqrt(3/K)) -> unit-variance outputs */
   float lm_head_gain;  /* larger gain on lm_head widens the logit spread */
+  int32_t tp_size;     /* 1 = single GPU */
+  int32_t tp_rank;     /* NX_TP_NCCL: this process's rank */
+  int32_t tp_mode;     /* NX_TP_NCCL / NX_TP_PEER / NX_TP_PEER_COLOCATED */
+  int32_t tp_pad;
+  uint8_t nccl_id[2][128]; /* NX_TP_NCCL: one communicator per lane (prefill, decode) */
 } nx_device_config;
 
 typedef struct nx_device nx_device;

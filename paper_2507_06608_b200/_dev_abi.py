@@ -18,7 +18,18 @@ class DeviceConfig(C.Structure):
     _fields_ = [("arch", Arch), ("device", C.c_int32), ("page_tokens", C.c_int32),
                 ("num_pages", C.c_int32), ("max_prefill_tokens", C.c_int32),
                 ("max_decode_batch", C.c_int32), ("green_contexts", C.c_int32),
-                ("weight_seed", C.c_uint64), ("weight_gain", C.c_float), ("lm_head_gain", C.c_float)]
+                ("weight_seed", C.c_uint64), ("weight_gain", C.c_float), ("lm_head_gain", C.c_float),
+                ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("tp_mode", C.c_int32), ("tp_pad", C.c_int32),
+                ("nccl_id", (C.c_uint8 * 128) * 2)]
+
+
+NX_TP_NCCL, NX_TP_PEER, NX_TP_PEER_COLOCATED = 0, 1, 2
+
+
+class TpShard(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("tp_size", "rank", "q_head0", "n_q_heads", "kv_head0", "n_kv_heads",
+                                         "ffn0", "ffn_local", "vocab0", "vocab_local", "vocab_valid",
+                                         "vocab_padded")]
 
 
 class DeviceInfo(C.Structure):
@@ -41,6 +52,8 @@ class KernelStats(C.Structure):
 
 
 PROTOS = {
+    "nx_tp_shard_plan": (C.c_int, [P(Arch), C.c_int32, C.c_int32, P(TpShard)]),
+    "nx_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
     "nx_device_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "nx_device_kernel_stats": (C.c_int, [C.c_void_p, P(KernelStats)]),
     "nx_device_reset_kernel_stats": (C.c_int, [C.c_void_p]),

@@ -10,6 +10,7 @@
 #include "capi_internal.hpp"
 #include "device.cuh"
 #include "model.cuh"
+#include "tp.cuh"
 
 struct nx_device {
   std::unique_ptr<nxd::Model> m;
@@ -58,6 +59,21 @@ int nx_device_create(const nx_device_config* cfg, nx_device** out) {
 }
 
 void nx_device_destroy(nx_device* dev) { delete dev; }
+
+int nx_tp_shard_plan(const nx_arch* arch, int32_t tp_size, int32_t rank, nx_tp_shard* out) {
+  return dguard([&] {
+    if (!arch || !out) throw std::invalid_argument("nx_tp_shard_plan: null argument");
+    *out = nxd::tp_plan(*arch, tp_size, rank);
+    return NX_OK;
+  });
+}
+
+int nx_nccl_unique_id(uint8_t out[128]) {
+  return dguard([&] {
+    nxd::Nccl::get().unique_id(out);
+    return NX_OK;
+  });
+}
 
 int nx_device_get_info(const nx_device* dev, nx_device_info* out) {
   std::memset(out, 0, sizeof(*out));

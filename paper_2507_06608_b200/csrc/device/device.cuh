@@ -107,11 +107,24 @@ cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* slot,
                           const float2* table, int n_heads, int n_kv_heads, int head_dim,
                           int page_tokens, __nv_bfloat16* kplane, __nv_bfloat16* vplane,
                           cudaStream_t s);
-// out[r] = argmax_j logits[r, j] (lowest index on ties); scratch holds
-// 16 float2 per row.
-cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, float2* scratch,
-                        cudaStream_t s);
+// out[r] = offset + argmax_{j < valid} logits[r * ld + j] (lowest index on
+// ties); pair_out (optional) gets (max, offset + argmax); scratch holds 16
+// float2 per row.
+cudaError_t argmax_rows(const float* logits, int n, int ld, int valid, int offset, int32_t* out,
+                        float2* pair_out, float2* scratch, cudaStream_t s);
+// TP: fold all-gathered [tp][rows] (max, global idx) pairs into tokens.
+cudaError_t argmax_fold(const float2* pairs, int tp, int rows, int32_t* out, cudaStream_t s);
 // Deterministic random bf16 fill: uniform(-scale, scale) + offset from a hash of (seed, i).
+// Local row r of a slice maps to global row global0[k] + (r - local0[k]) for
+// the last segment k with local0[k] <= r (QKV shards have three segments).
+struct RowMap {
+  int nseg = 1;
+  int local0[3] = {0, 0, 0};
+  long long global0[3] = {0, 0, 0};
+};
+cudaError_t fill_random_slice(__nv_bfloat16* p, int rows, int cols, const RowMap& m,
+                              size_t full_cols, size_t col0, uint64_t seed, float scale,
+                              float offset, cudaStream_t s);
 cudaError_t fill_random(__nv_bfloat16* p, size_t n, uint64_t seed, float scale, float offset,
                         cudaStream_t s);
 

@@ -146,12 +146,12 @@ __device__ __forceinline__ void arg_better(float& best, int& idx, float v, int i
   }
 }
 
-__global__ void argmax_partial_kernel(const float* __restrict__ logits, int vocab,
+__global__ void argmax_partial_kernel(const float* __restrict__ logits, int ld, int valid,
                                       float2* __restrict__ part) {
   const int row = blockIdx.y, chunk = blockIdx.x;
-  const int per = (vocab + kArgChunks - 1) / kArgChunks;
-  const int lo = chunk * per, hi = min(vocab, lo + per);
-  const float* r = logits + static_cast<size_t>(row) * vocab;
+  const int per = (valid + kArgChunks - 1) / kArgChunks;
+  const int lo = chunk * per, hi = min(valid, lo + per);
+  const float* r = logits + static_cast<size_t>(row) * ld;
   float best = -FLT_MAX;
   int idx = 0x7fffffff;
   for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) arg_better(best, idx, r[i], i);
@@ -171,7 +171,8 @@ __global__ void argmax_partial_kernel(const float* __restrict__ logits, int voca
   }
 }
 
-__global__ void argmax_final_kernel(const float2* __restrict__ part, int rows, int32_t* __restrict__ out) {
+__global__ void argmax_final_kernel(const float2* __restrict__ part, int rows, int offset,
+                                    int32_t* __restrict__ out, float2* __restrict__ pair_out) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -185,7 +186,24 @@ __global__ void argmax_final_kernel(const float2* __restrict__ part, int rows, i
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
     arg_better(best, idx, __shfl_xor_sync(0xffffffff, best, o), __shfl_xor_sync(0xffffffff, idx, o));
-  if (lane == 0) out[row] = idx;
+  if (lane == 0) {
+    if (out) out[row] = idx + offset;
+    if (pair_out) pair_out[row] = make_float2(best, __int_as_float(idx + offset));
+  }
+}
+
+// TP: fold the all-gathered [tp][rows] (max, global idx) pairs.
+__global__ void argmax_fold_kernel(const float2* __restrict__ pairs, int tp, int rows,
+                                   int32_t* __restrict__ out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  float best = -FLT_MAX;
+  int idx = 0x7fffffff;
+  for (int r = 0; r < tp; ++r) {
+    const float2 p = pairs[static_cast<size_t>(r) * rows + row];
+    arg_better(best, idx, p.x, __float_as_int(p.y));
+  }
+  out[row] = idx;
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -205,7 +223,35 @@ __global__ void fill_random_kernel(__nv_bfloat16* p, size_t n, uint64_t seed, fl
   }
 }
 
+// Row/column slice of a larger logical matrix: element (r, c) of the slice
+// takes the value of global element (rowmap(r), col0 + c), so a TP shard holds
+// exactly the corresponding entries of the unsharded model.
+__global__ void fill_random_slice_kernel(__nv_bfloat16* p, int rows, int cols, RowMap m,
+                                         size_t full_cols, size_t col0, uint64_t seed,
+                                         float scale, float offset) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int lr = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+    int sg = 0;
+    for (int k = 1; k < m.nseg; ++k)
+      if (lr >= m.local0[k]) sg = k;
+    const size_t gr = static_cast<size_t>(m.global0[sg] + (lr - m.local0[sg]));
+    const uint64_t h = mix64(seed ^ mix64(gr * full_cols + col0 + c));
+    const float u = static_cast<float>(h >> 40) * (1.0f / 16777216.0f);
+    p[i] = __float2bfloat16(offset + scale * (2.f * u - 1.f));
+  }
+}
+
 }  // namespace
+
+cudaError_t fill_random_slice(__nv_bfloat16* p, int rows, int cols, const RowMap& m,
+                              size_t full_cols, size_t col0, uint64_t seed, float scale,
+                              float offset, cudaStream_t s) {
+  fill_random_slice_kernel<<<1184, 256, 0, s>>>(p, rows, cols, m, full_cols, col0, seed, scale,
+                                                offset);
+  return cudaGetLastError();
+}
 
 cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int hidden,
                   __nv_bfloat16* out, cudaStream_t s) {
@@ -243,12 +289,19 @@ cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* slot,
   return cudaGetLastError();
 }
 
-cudaError_t argmax_rows(const float* logits, int n, int vocab, int32_t* out, float2* scratch,
-                        cudaStream_t s) {
+cudaError_t argmax_rows(const float* logits, int n, int ld, int valid, int offset, int32_t* out,
+                        float2* pair_out, float2* scratch, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   g_kernel_launches += 2;
-  argmax_partial_kernel<<<dim3(kArgChunks, n), 256, 0, s>>>(logits, vocab, scratch);
-  argmax_final_kernel<<<(n + 7) / 8, 256, 0, s>>>(scratch, n, out);
+  argmax_partial_kernel<<<dim3(kArgChunks, n), 256, 0, s>>>(logits, ld, valid, scratch);
+  argmax_final_kernel<<<(n + 7) / 8, 256, 0, s>>>(scratch, n, offset, out, pair_out);
+  return cudaGetLastError();
+}
+
+cudaError_t argmax_fold(const float2* pairs, int tp, int rows, int32_t* out, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  ++g_kernel_launches;
+  argmax_fold_kernel<<<(rows + 127) / 128, 128, 0, s>>>(pairs, tp, rows, out);
   return cudaGetLastError();
 }
 

@@ -117,7 +117,22 @@ Partitions::Pick Partitions::pick(int lane_kind, int sm_pct) const {
 // ---------------------------------------------------------------------------
 // Model.
 // ---------------------------------------------------------------------------
-Model::Model(const nx_device_config& cfg) : cfg_(cfg), a_(cfg.arch) {
+namespace {
+// Makes `dev` current for the scope (ranks of one process live on several GPUs).
+struct DevGuard {
+  int prev = -1, dev;
+  explicit DevGuard(int d) : dev(d) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+Model::Model(const nx_device_config& cfg, std::shared_ptr<PeerGroup> group)
+    : cfg_(cfg), a_(cfg.arch), group_(std::move(group)), dev_(cfg.device) {
   if (a_.head_dim != 128) throw std::invalid_argument("head_dim must be 128");
   if (a_.hidden % 128 || a_.ffn % 64 || a_.vocab % 128 || (2 * a_.ffn) % 128)
     throw std::invalid_argument("hidden/vocab must be multiples of 128, ffn of 64");
@@ -133,12 +148,41 @@ Model::Model(const nx_device_config& cfg) : cfg_(cfg), a_(cfg.arch) {
   ck(cudaGetDeviceProperties(&prop, cfg.device), "props");
   if (prop.major != 10) throw NoDevice("sm_100 device required");
   parts_.init(cfg.device, cfg.green_contexts != 0);
-  qkv_rows_ = (a_.n_heads + 2 * a_.n_kv_heads) * a_.head_dim;
-  attn_cols_ = a_.n_heads * a_.head_dim;
+  tp_ = cfg.tp_size > 1 ? cfg.tp_size : 1;
+  rank_ = tp_ > 1 ? cfg.tp_rank : 0;
+  const nx_tp_shard sh = tp_plan(a_, tp_, rank_);
+  hq_ = sh.n_q_heads;
+  hkv_ = sh.n_kv_heads;
+  ffn_ = sh.ffn_local;
+  vocab_l_ = tp_ > 1 ? sh.vocab_local : a_.vocab;
+  vocab_valid_ = tp_ > 1 ? sh.vocab_valid : a_.vocab;
+  vocab0_ = tp_ > 1 ? sh.vocab0 : 0;
+  const bool peer_mode = tp_ > 1 && (cfg.tp_mode == NX_TP_PEER || cfg.tp_mode == NX_TP_PEER_COLOCATED);
+  if (tp_ > 1 && !peer_mode) {
+    if (cfg.tp_mode != NX_TP_NCCL) throw std::invalid_argument("unknown tp_mode");
+    Nccl& nc = Nccl::get();
+    comm_[0] = nc.comm_init(tp_, cfg.nccl_id[0], rank_);
+    comm_[1] = nc.comm_init(tp_, cfg.nccl_id[1], rank_);
+  }
+  if (peer_mode && !group_) {
+    // rank 0 of a one-process group: owns the group and builds ranks 1..tp-1
+    if (cfg.tp_rank != 0) throw std::invalid_argument("peer TP group is created through rank 0");
+    if (cfg.tp_mode == NX_TP_PEER && cfg.device + tp_ > ndev)
+      throw NoDevice("NX_TP_PEER needs tp_size GPUs starting at `device`");
+    group_ = std::make_shared<PeerGroup>(tp_);
+  }
+  qkv_rows_ = (hq_ + 2 * hkv_) * a_.head_dim;
+  attn_cols_ = hq_ * a_.head_dim;
   alloc_weights();
   alloc_kv();
   lanes_[0].init(this, cfg.max_prefill_tokens);
   lanes_[1].init(this, cfg.max_decode_batch);
+  lanes_[0].slot_index = 0;
+  lanes_[1].slot_index = 1;
+  if (group_) {
+    group_->register_lane(rank_, 0, static_cast<size_t>(lanes_[0].t_max) * a_.hidden);
+    group_->register_lane(rank_, 1, static_cast<size_t>(lanes_[1].t_max) * a_.hidden);
+  }
   // RoPE inverse frequencies theta^(-2i/hd), computed in double, stored fp32.
   std::vector<float> inv(a_.head_dim / 2);
   for (int i = 0; i < a_.head_dim / 2; ++i)
@@ -148,10 +192,42 @@ Model::Model(const nx_device_config& cfg) : cfg_(cfg), a_(cfg.arch) {
   ck(cudaMemcpy(inv_freq_, inv.data(), inv.size() * sizeof(float), cudaMemcpyHostToDevice),
      "copy inv_freq");
   ck(cudaDeviceSynchronize(), "init sync");
+  if (group_ && rank_ == 0) {
+    for (int r = 1; r < tp_; ++r) {
+      nx_device_config c = cfg_;
+      c.tp_rank = r;
+      if (cfg_.tp_mode == NX_TP_PEER) c.device = cfg_.device + r;
+      peers_.push_back(std::make_unique<Model>(c, group_));
+    }
+    if (cfg_.tp_mode == NX_TP_PEER)  // every rank reads every other rank's slots
+      for (int i = 0; i < tp_; ++i) {
+        ck(cudaSetDevice(cfg_.device + i), "cudaSetDevice");
+        for (int j = 0; j < tp_; ++j) {
+          if (i == j) continue;
+          int ok = 0;
+          ck(cudaDeviceCanAccessPeer(&ok, cfg_.device + i, cfg_.device + j), "peer query");
+          if (!ok) throw NoDevice("GPUs of the TP group lack peer access");
+          const cudaError_t e = cudaDeviceEnablePeerAccess(cfg_.device + j, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else ck(e, "enable peer access");
+        }
+      }
+    ck(cudaSetDevice(dev_), "cudaSetDevice");
+  }
+}
+
+void Model::all_reduce(LaneWs& ws, __nv_bfloat16* x, size_t n) {
+  if (group_) group_->all_reduce_bf16(rank_, ws.slot_index, x, n, ws.stream);
+  else Nccl::get().all_reduce_bf16(comm_[ws.slot_index], x, n, ws.stream);
 }
 
 Model::~Model() {
+  peers_.clear();
+  DevGuard g(dev_);
   cudaDeviceSynchronize();
+  for (void* c : comm_)
+    if (c) Nccl::get().destroy(c);
+  if (group_) group_->release_rank(rank_);
   for (void* p : allocs_) cudaFree(p);
   for (auto& l : lanes_) l.release();
 }
@@ -165,51 +241,75 @@ __nv_bfloat16* Model::dalloc_bf16(size_t n) {
 
 void Model::alloc_weights() {
   const size_t d = a_.hidden, L = a_.n_layers;
+  // Same seed sequence on every rank: a TP shard is generated as the exact
+  // slice of the unsharded model's tensors (fill_random_slice).
   uint64_t seed = cfg_.weight_seed;
   auto next_seed = [&]() { return seed = seed * 6364136223846793005ULL + 1442695040888963407ULL; };
   const float g = cfg_.weight_gain > 0 ? cfg_.weight_gain : 1.0f;
   auto uni = [&](size_t k) { return g * std::sqrt(3.0f / static_cast<float>(k)); };
+  const nx_tp_shard sh = tp_plan(a_, tp_, rank_);
+  const int hd = a_.head_dim;
+  // row maps of the column-parallel tensors
+  RowMap qkv_map;  // [q heads | k heads | v heads] -> this rank's heads of each
+  qkv_map.nseg = 3;
+  qkv_map.local0[1] = hq_ * hd;
+  qkv_map.local0[2] = (hq_ + hkv_) * hd;
+  qkv_map.global0[0] = static_cast<long long>(sh.q_head0) * hd;
+  qkv_map.global0[1] = static_cast<long long>(a_.n_heads + sh.kv_head0) * hd;
+  qkv_map.global0[2] = static_cast<long long>(a_.n_heads + a_.n_kv_heads + sh.kv_head0) * hd;
+  RowMap gu_map;  // 128-row blocks of (64 gate | 64 up) features
+  gu_map.global0[0] = 2LL * sh.ffn0;
+  RowMap lm_map;
+  lm_map.global0[0] = sh.vocab0;
+  const RowMap whole;
   // staging buffer for the logical (row-major) random init before packing
   const size_t max_mat = std::max({static_cast<size_t>(qkv_rows_) * d, d * attn_cols_,
-                                   2 * static_cast<size_t>(a_.ffn) * d,
-                                   static_cast<size_t>(a_.vocab) * d});
+                                   2 * static_cast<size_t>(ffn_) * d,
+                                   static_cast<size_t>(vocab_l_) * d});
   __nv_bfloat16* stage = nullptr;
   ck(cudaMalloc(&stage, max_mat * 2), "weight staging");
-  auto plain = [&](size_t n, float scale, float offset) {
+  auto plain = [&](size_t n, float scale, float offset, const RowMap& m = RowMap()) {
     __nv_bfloat16* p = dalloc_bf16(n);
-    ck(fill_random(p, n, next_seed(), scale, offset, nullptr), "init weights");
+    ck(fill_random_slice(p, static_cast<int>(n), 1, m, 1, 0, next_seed(), scale, offset, nullptr),
+       "init weights");
     weight_bytes_ += n * 2;
     return p;
   };
-  auto packed = [&](int rows, int K, float scale) {
+  auto packed = [&](int rows, int K, float scale, const RowMap& m, size_t full_k, size_t k0) {
     const size_t n = static_cast<size_t>(rows) * K;
-    ck(fill_random(stage, n, next_seed(), scale, 0.f, nullptr), "init weights");
+    ck(fill_random_slice(stage, rows, K, m, full_k, k0, next_seed(), scale, 0.f, nullptr),
+       "init weights");
     __nv_bfloat16* p = dalloc_bf16(packed_weight_elems(rows, K));
     ck(pack_weights(stage, p, rows, K, nullptr), "pack weights");
     weight_bytes_ += n * 2;
     return p;
   };
-  emb_ = plain(static_cast<size_t>(a_.vocab) * d, 1.0f, 0.f);
+  emb_ = dalloc_bf16(static_cast<size_t>(a_.vocab) * d);
+  ck(fill_random(emb_, static_cast<size_t>(a_.vocab) * d, next_seed(), 1.0f, 0.f, nullptr),
+     "init weights");
+  weight_bytes_ += static_cast<size_t>(a_.vocab) * d * 2;
+  const size_t q_cols = static_cast<size_t>(a_.n_heads) * hd;
   layers_.resize(L);
   for (size_t l = 0; l < L; ++l) {
     LayerW& w = layers_[l];
     w.attn_norm = plain(d, 0.1f, 1.0f);
-    w.qkv = packed(qkv_rows_, static_cast<int>(d), uni(d));
-    w.qkv_bias = a_.qkv_bias ? plain(qkv_rows_, 0.1f, 0.f) : nullptr;
-    w.o = packed(static_cast<int>(d), attn_cols_, uni(attn_cols_));
+    w.qkv = packed(qkv_rows_, static_cast<int>(d), uni(d), qkv_map, d, 0);
+    w.qkv_bias = a_.qkv_bias ? plain(qkv_rows_, 0.1f, 0.f, qkv_map) : nullptr;
+    w.o = packed(static_cast<int>(d), attn_cols_, uni(q_cols), whole, q_cols,
+                 static_cast<size_t>(sh.q_head0) * hd);
     w.ffn_norm = plain(d, 0.1f, 1.0f);
-    w.gate_up = packed(2 * a_.ffn, static_cast<int>(d), uni(d));
-    w.down = packed(static_cast<int>(d), a_.ffn, uni(a_.ffn) * 2.0f);
+    w.gate_up = packed(2 * ffn_, static_cast<int>(d), uni(d), gu_map, d, 0);
+    w.down = packed(static_cast<int>(d), ffn_, uni(a_.ffn) * 2.0f, whole, a_.ffn, sh.ffn0);
   }
   final_norm_ = plain(d, 0.1f, 1.0f);
   const float lm_gain = cfg_.lm_head_gain > 0 ? cfg_.lm_head_gain : 1.0f;
-  lm_head_ = packed(a_.vocab, static_cast<int>(d), lm_gain * std::sqrt(3.0f / d));
+  lm_head_ = packed(vocab_l_, static_cast<int>(d), lm_gain * std::sqrt(3.0f / d), lm_map, d, 0);
   ck(cudaDeviceSynchronize(), "weights");
   cudaFree(stage);
 }
 
 void Model::alloc_kv() {
-  plane_elems_ = static_cast<size_t>(cfg_.num_pages) * a_.n_kv_heads * cfg_.page_tokens *
+  plane_elems_ = static_cast<size_t>(cfg_.num_pages) * hkv_ * cfg_.page_tokens *
                  a_.head_dim;
   const size_t total = plane_elems_ * 2 * a_.n_layers;
   kv_ = dalloc_bf16(total);
@@ -234,10 +334,11 @@ void LaneWs::init(Model* m, int max_tokens) {
   h = static_cast<__nv_bfloat16*>(alloc(T * a.hidden * 2));
   qkv = static_cast<__nv_bfloat16*>(alloc(T * m->qkv_rows_ * 2));
   attn = static_cast<__nv_bfloat16*>(alloc(T * m->attn_cols_ * 2));
-  act = static_cast<__nv_bfloat16*>(alloc(T * a.ffn * 2));
+  act = static_cast<__nv_bfloat16*>(alloc(T * m->ffn_ * 2));
   sample_cap = std::min<int>(t_max, 256);
   hs = static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(sample_cap) * a.hidden * 2));
-  logits = static_cast<float*>(alloc(static_cast<size_t>(sample_cap) * a.vocab * 4));
+  logits = static_cast<float*>(alloc(static_cast<size_t>(sample_cap) * m->vocab_l_ * 4));
+  tp_pairs = static_cast<float2*>(alloc(static_cast<size_t>(sample_cap) * (m->tp_ + 1) * sizeof(float2)));
   rope_cs = static_cast<float2*>(alloc(T * (a.head_dim / 2) * sizeof(float2)));
   ws_bytes = 96u << 20;
   ws = static_cast<float*>(alloc(ws_bytes));
@@ -261,7 +362,7 @@ void LaneWs::init(Model* m, int max_tokens) {
     if (!encode_kmajor(&map_h[i], h, T, a.hidden, static_cast<size_t>(a.hidden) * 2, bn) ||
         !encode_kmajor(&map_attn[i], attn, T, m->attn_cols_, static_cast<size_t>(m->attn_cols_) * 2,
                        bn) ||
-        !encode_kmajor(&map_act[i], act, T, a.ffn, static_cast<size_t>(a.ffn) * 2, bn) ||
+        !encode_kmajor(&map_act[i], act, T, m->ffn_, static_cast<size_t>(m->ffn_) * 2, bn) ||
         !encode_kmajor(&map_hs[i], hs, sample_cap, a.hidden, static_cast<size_t>(a.hidden) * 2, bn))
       throw std::runtime_error("cuTensorMapEncodeTiled failed (activations)");
   }
@@ -282,6 +383,8 @@ static int bn_index(int bn) { return bn == 32 ? 0 : bn == 64 ? 1 : bn == 128 ? 2
 // Forward.
 // ---------------------------------------------------------------------------
 void Model::launch(int slot, const nxb::ExecBatch& b) {
+  for (auto& p : peers_) p->launch(slot, b);
+  DevGuard guard(dev_);
   LaneWs& ws = lanes_[slot];
   const Partitions::Pick pk = parts_.pick(b.lane_kind, b.sm_pct);
   ws.stream = pk.stream;
@@ -310,7 +413,7 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   const size_t o_rows = carve(n_sample * 4 + 4);
   int max_work = 0;
   for (const auto& m : b.members)
-    max_work += (m.n_tokens * (a_.n_heads / a_.n_kv_heads) + 63) / 64;
+    max_work += (m.n_tokens * (hq_ / hkv_) + 63) / 64;
   const size_t o_work = carve(static_cast<size_t>(max_work) * sizeof(int2) + 8);
   int32_t* tok = reinterpret_cast<int32_t*>(hp + o_tok);
   int32_t* pos = reinterpret_cast<int32_t*>(hp + o_pos);
@@ -319,7 +422,7 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   int32_t* pages = reinterpret_cast<int32_t*>(hp + o_pages);
   int32_t* rows = reinterpret_cast<int32_t*>(hp + o_rows);
   int2* work = reinterpret_cast<int2*>(hp + o_work);
-  const int group = a_.n_heads / a_.n_kv_heads;
+  const int group = hq_ / hkv_;
   int t = 0, pg = 0, ns = 0, nw = 0;
   ws.dec_seq_count = 0;
   ws.max_dec_kv = 0;
@@ -410,15 +513,15 @@ void Model::forward(LaneWs& ws) {
   };
   auto gflops = [&](double rows, double K) { return 2.0 * Td * rows * K; };
   AttnGeom g;
-  g.n_heads = a_.n_heads;
-  g.n_kv_heads = a_.n_kv_heads;
-  g.group = a_.n_heads / a_.n_kv_heads;
+  g.n_heads = hq_;
+  g.n_kv_heads = hkv_;
+  g.group = hq_ / hkv_;
   g.head_dim = a_.head_dim;
   g.page_tokens = cfg_.page_tokens;
   g.qkv_stride = qkv_rows_;
   g.out_stride = attn_cols_;
   g.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(a_.head_dim));
-  const double kvtok = 2.0 * a_.n_kv_heads * a_.head_dim * 2;  // K+V bytes per token per layer
+  const double kvtok = 2.0 * hkv_ * a_.head_dim * 2;  // K+V bytes per token per layer
   const double qo = 2.0 * attn_cols_ * 2;                       // q in + out per token
   timed(NX_K_OTHER, Td * d * 2 + Td * 4, 0, [&] { ck(embed(ws.d_tok, T, emb_, d, ws.x, s), "embed"); });
   timed(NX_K_OTHER, Td * a_.head_dim * 4, 0, [&] {
@@ -437,7 +540,7 @@ void Model::forward(LaneWs& ws) {
          "qkv gemm");
     });
     timed(NX_K_OTHER, Td * qkv_rows_ * 4, 0, [&] {
-      ck(rope_kv_write(ws.qkv, T, ws.d_slot, ws.rope_cs, a_.n_heads, a_.n_kv_heads, a_.head_dim,
+      ck(rope_kv_write(ws.qkv, T, ws.d_slot, ws.rope_cs, hq_, hkv_, a_.head_dim,
                        cfg_.page_tokens, kplane, vplane, s),
          "rope");
     });
@@ -456,24 +559,29 @@ void Model::forward(LaneWs& ws) {
                                    ws.d_pages, ws.attn, s),
                  "prefill attention");
             });
+    // Row-parallel under TP: rank 0 adds the residual, the others store
+    // their partial; the all-reduce then yields x + sum_r o_r on every rank.
+    const int res_mode = (tp_ == 1 || rank_ == 0) ? kEpiResidual : kEpiStore;
     timed(gk, gbytes(d, attn_cols_, 2, true), gflops(d, attn_cols_), [&] {
-      ck(gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, kEpiResidual, ws.x, d, nullptr, ws.x,
+      ck(gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x,
               d, ws.ws, ws.ws_bytes, sm, s),
          "o gemm");
     });
+    if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
     timed(NX_K_OTHER, Td * d * 4, 0, [&] {
       ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
     });
-    timed(gk, gbytes(2.0 * a_.ffn, d, 1, false), gflops(2.0 * a_.ffn, d), [&] {
-      ck(gemm(w.gate_up, ws.map_h[bi], bn, 2 * a_.ffn, T, d, kEpiSwiGLU, ws.act, a_.ffn, nullptr,
+    timed(gk, gbytes(2.0 * ffn_, d, 1, false), gflops(2.0 * ffn_, d), [&] {
+      ck(gemm(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr,
               nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
          "gate/up gemm");
     });
-    timed(gk, gbytes(d, a_.ffn, 2, true), gflops(d, a_.ffn), [&] {
-      ck(gemm(w.down, ws.map_act[bi], bn, d, T, a_.ffn, kEpiResidual, ws.x, d, nullptr, ws.x, d,
+    timed(gk, gbytes(d, ffn_, 2, true), gflops(d, ffn_), [&] {
+      ck(gemm(w.down, ws.map_act[bi], bn, d, T, ffn_, res_mode, ws.x, d, nullptr, ws.x, d,
               ws.ws, ws.ws_bytes, sm, s),
          "down gemm");
     });
+    if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
   }
   // lm_head over the sampled rows, in chunks of the logits buffer.
   ws.d_out_tokens = ws.logits_tokens_dev();
@@ -484,16 +592,31 @@ void Model::forward(LaneWs& ws) {
       ck(rmsnorm(ws.x, ws.d_rows + r0, n, d, final_norm_, a_.rms_eps, ws.hs, s), "final norm");
     });
     const int sbn = gemm_pick_bn(n);
-    timed(gk, static_cast<double>(a_.vocab) * d * 2 + nd * d * 2 + nd * a_.vocab * 4,
-          2.0 * nd * a_.vocab * d, [&] {
-            ck(gemm(lm_head_, ws.map_hs[bn_index(sbn)], sbn, a_.vocab, n, d, kEpiF32, ws.logits,
-                    a_.vocab, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+    timed(gk, static_cast<double>(vocab_l_) * d * 2 + nd * d * 2 + nd * vocab_l_ * 4,
+          2.0 * nd * vocab_l_ * d, [&] {
+            ck(gemm(lm_head_, ws.map_hs[bn_index(sbn)], sbn, vocab_l_, n, d, kEpiF32, ws.logits,
+                    vocab_l_, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
                "lm_head gemm");
           });
-    timed(NX_K_OTHER, nd * a_.vocab * 4, 0,
-          [&] { ck(argmax_rows(ws.logits, n, a_.vocab, ws.d_out_tokens + r0,
-                            reinterpret_cast<float2*>(ws.part_ml), s),
-               "argmax"); });
+    timed(NX_K_OTHER, nd * vocab_l_ * 4, 0, [&] {
+      if (tp_ == 1) {
+        ck(argmax_rows(ws.logits, n, vocab_l_, vocab_l_, 0, ws.d_out_tokens + r0, nullptr,
+                       reinterpret_cast<float2*>(ws.part_ml), s),
+           "argmax");
+        return;
+      }
+      // vocab-parallel: local (max, global idx) pairs -> all-gather -> fold
+      float2* mine = ws.tp_pairs + static_cast<size_t>(n) * tp_;
+      ck(argmax_rows(ws.logits, n, vocab_l_, vocab_valid_, vocab0_, nullptr, mine,
+                     reinterpret_cast<float2*>(ws.part_ml), s),
+         "argmax");
+      if (group_) {
+        group_->argmax_gather(rank_, ws.slot_index, mine, n, ws.d_out_tokens + r0, s);
+        return;
+      }
+      Nccl::get().all_gather_f2(comm_[ws.slot_index], mine, ws.tp_pairs, 2 * static_cast<size_t>(n), s);
+      ck(argmax_fold(ws.tp_pairs, tp_, n, ws.d_out_tokens + r0, s), "argmax fold");
+    });
   }
 }
 
@@ -506,6 +629,9 @@ int32_t* LaneWs::logits_tokens_dev() {
 }
 
 bool Model::done(int slot) {
+  for (auto& p : peers_)
+    if (!p->done(slot)) return false;
+  DevGuard guard(dev_);
   LaneWs& ws = lanes_[slot];
   if (!ws.pending) return true;
   const cudaError_t e = cudaEventQuery(ws.ev_end);
@@ -516,6 +642,8 @@ bool Model::done(int slot) {
 }
 
 void Model::wait(int slot) {
+  for (auto& p : peers_) p->wait(slot);
+  DevGuard guard(dev_);
   LaneWs& ws = lanes_[slot];
   if (!ws.pending) return;
   ck(cudaEventSynchronize(ws.ev_end), "device batch");
@@ -524,6 +652,8 @@ void Model::wait(int slot) {
 
 void Model::finish(LaneWs& ws) {
   ws.pending = false;
+  if (group_ && group_->error())
+    throw std::runtime_error("TP peer collective timed out (a rank never arrived)");
   kstats_.batches += 1;
   ws.sampled.assign(ws.out_host, ws.out_host + ws.n_sample);
   float ms = 0.f;
@@ -546,12 +676,31 @@ void Model::finish(LaneWs& ws) {
 }
 
 void Model::copy_logits(int slot, float* host, size_t n_floats) {
+  DevGuard guard(dev_);
   LaneWs& ws = lanes_[slot];
-  const size_t want = std::min<size_t>(n_floats, static_cast<size_t>(std::min(ws.n_sample, ws.sample_cap)) * a_.vocab);
-  ck(cudaMemcpy(host, ws.logits, want * 4, cudaMemcpyDeviceToHost), "logits d2h");
+  const size_t rows = static_cast<size_t>(std::min(ws.n_sample, ws.sample_cap));
+  if (!group_) {
+    const size_t want = std::min<size_t>(n_floats, rows * vocab_l_);
+    ck(cudaMemcpy(host, ws.logits, want * 4, cudaMemcpyDeviceToHost), "logits d2h");
+    return;
+  }
+  // one-process TP group: stitch every rank's vocab slice into [rows][vocab]
+  std::vector<float> part(rows * vocab_l_);
+  for (int r = 0; r < tp_; ++r) {
+    Model* m = r == 0 ? this : peers_[r - 1].get();
+    DevGuard g(m->dev_);
+    ck(cudaMemcpy(part.data(), m->lanes_[slot].logits, part.size() * 4, cudaMemcpyDeviceToHost),
+       "logits d2h");
+    for (size_t i = 0; i < rows; ++i)
+      for (int j = 0; j < m->vocab_valid_; ++j) {
+        const size_t dst = i * a_.vocab + m->vocab0_ + j;
+        if (dst < n_floats) host[dst] = part[i * vocab_l_ + j];
+      }
+  }
 }
 
 size_t Model::weight_to_host(int tensor, int layer, void* host, size_t cap) const {
+  DevGuard guard(dev_);
   const size_t d = a_.hidden;
   if (tensor != 0 && tensor != 8 && tensor != 9 && (layer < 0 || layer >= a_.n_layers))
     throw std::invalid_argument("unknown layer");
@@ -565,10 +714,10 @@ size_t Model::weight_to_host(int tensor, int layer, void* host, size_t cap) cons
     case 3: p = layers_[layer].qkv_bias; elems = a_.qkv_bias ? qkv_rows_ : 0; break;
     case 4: p = layers_[layer].o; rows = static_cast<int>(d); K = attn_cols_; break;
     case 5: p = layers_[layer].ffn_norm; elems = d; break;
-    case 6: p = layers_[layer].gate_up; rows = 2 * a_.ffn; K = static_cast<int>(d); break;
-    case 7: p = layers_[layer].down; rows = static_cast<int>(d); K = a_.ffn; break;
+    case 6: p = layers_[layer].gate_up; rows = 2 * ffn_; K = static_cast<int>(d); break;
+    case 7: p = layers_[layer].down; rows = static_cast<int>(d); K = ffn_; break;
     case 8: p = final_norm_; elems = d; break;
-    case 9: p = lm_head_; rows = a_.vocab; K = static_cast<int>(d); break;
+    case 9: p = lm_head_; rows = vocab_l_; K = static_cast<int>(d); break;
     default: throw std::invalid_argument("unknown tensor");
   }
   if (rows) elems = static_cast<size_t>(rows) * K;

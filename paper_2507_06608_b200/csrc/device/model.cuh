@@ -10,6 +10,8 @@
 
 #include "device.cuh"
 #include "executor.hpp"
+#include "tp.cuh"
+#include <memory>
 #include "nexus_b200.h"
 
 namespace nxd {
@@ -51,6 +53,8 @@ struct LaneWs {
                 *hs = nullptr;
   float* logits = nullptr;
   float2* rope_cs = nullptr;  // per-batch RoPE table [t_max][64]
+  float2* tp_pairs = nullptr;  // TP: (max, argmax) per sampled row, gathered [tp][rows]
+  int slot_index = 0;
   int sample_cap = 0;
   float* ws = nullptr;
   size_t ws_bytes = 0;
@@ -98,7 +102,9 @@ struct LayerW {
 
 class Model : public nxb::Executor {
  public:
-  explicit Model(const nx_device_config& cfg);
+  // group: the peer-memory TP group this rank belongs to (NX_TP_PEER*); rank 0
+  // creates it and the other ranks' Models, and fans every batch out to them.
+  explicit Model(const nx_device_config& cfg, std::shared_ptr<PeerGroup> group = nullptr);
   ~Model() override;
 
   void launch(int slot, const nxb::ExecBatch& b) override;
@@ -137,6 +143,15 @@ class Model : public nxb::Executor {
   nx_device_config cfg_;
   nx_arch a_;
   int qkv_rows_ = 0, attn_cols_ = 0;
+  // tensor-parallel shard (tp_ = 1: whole model on this GPU)
+  int tp_ = 1, rank_ = 0;
+  int hq_ = 0, hkv_ = 0, ffn_ = 0;        // local q heads, kv heads, ffn features
+  int vocab_l_ = 0, vocab_valid_ = 0, vocab0_ = 0;  // local lm_head rows (padded), valid, offset
+  void* comm_[2] = {nullptr, nullptr};    // NCCL communicator per lane
+  std::shared_ptr<PeerGroup> group_;      // peer-memory TP group (one process)
+  std::vector<std::unique_ptr<Model>> peers_;  // ranks 1..tp-1 (rank 0 only)
+  int dev_ = 0;
+  void all_reduce(LaneWs& ws, __nv_bfloat16* x, size_t n);
   Partitions parts_;
   std::vector<void*> allocs_;
   __nv_bfloat16 *emb_ = nullptr, *final_norm_ = nullptr, *lm_head_ = nullptr, *kv_ = nullptr;

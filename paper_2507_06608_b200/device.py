@@ -3,12 +3,15 @@ raw device buffers and the single-op GEMM entry point (C-ABI, no torch)."""
 from __future__ import annotations
 
 import ctypes as C
+import importlib.util
+import os
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _abi
-from ._dev_abi import Arch, BatchDesc, DeviceConfig, DeviceInfo, KernelStats
+from ._dev_abi import (NX_TP_NCCL, NX_TP_PEER, NX_TP_PEER_COLOCATED, Arch, BatchDesc, DeviceConfig,  # noqa: F401
+                       DeviceInfo, KernelStats, TpShard)
 
 W_EMBED, W_ATTN_NORM, W_QKV, W_QKV_BIAS, W_O, W_FFN_NORM, W_GATE_UP, W_DOWN, W_FINAL_NORM, W_LM_HEAD = range(10)
 
@@ -62,15 +65,62 @@ def arch_preset(name: str, **over) -> Arch:
     return arch(**kw)
 
 
+def _prefer_torch_nccl():
+    """Point NX_NCCL_LIB at the libnccl torch links (the pip nvidia-nccl
+    wheel) so both share one NCCL; loading the system copy first under the
+    same soname would break a later `import torch`."""
+    if os.environ.get("NX_NCCL_LIB"):
+        return
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        so = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(so):
+            os.environ["NX_NCCL_LIB"] = so
+            return
+
+
+_prefer_torch_nccl()
+
+
+def shard_plan(a: Arch, tp_size: int, rank: int) -> TpShard:
+    """nx_tp_shard_plan: the heads / ffn features / vocab rows rank owns."""
+    s = TpShard()
+    _check(lib().nx_tp_shard_plan(C.byref(a), tp_size, rank, C.byref(s)))
+    return s
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().nx_nccl_unique_id(buf))
+    return bytes(buf)
+
+
 class Device:
     """nx_device: weights + paged KV cache + per-lane workspaces + SM layouts."""
 
     def __init__(self, a: Arch, *, num_pages=4096, page_tokens=16, max_prefill_tokens=2048 + 64,
                  max_decode_batch=64, green_contexts=True, seed=1, weight_gain=1.0, lm_head_gain=4.0,
-                 device=0):
+                 device=0, tp_size=1, tp_rank=0, tp_mode=NX_TP_NCCL, nccl_ids=None):
+        """tp_size > 1, tp_mode NX_TP_NCCL: this process holds shard ``tp_rank``
+        of a Megatron-style tensor-parallel model; ``nccl_ids`` are the two
+        128-byte ids from ``nccl_unique_id()`` on rank 0 (one communicator per
+        lane), shared by the caller (e.g. torch.distributed.broadcast_object_list).
+        tp_mode NX_TP_PEER / NX_TP_PEER_COLOCATED: this Device drives all
+        ranks (GPUs device..device+tp-1, or all on ``device``) with
+        peer-memory collectives."""
         self.arch = a
         cfg = DeviceConfig(a, device, page_tokens, num_pages, max_prefill_tokens, max_decode_batch,
-                           1 if green_contexts else 0, seed, weight_gain, lm_head_gain)
+                           1 if green_contexts else 0, seed, weight_gain, lm_head_gain, tp_size, tp_rank,
+                           tp_mode)
+        if tp_size > 1 and tp_mode == NX_TP_NCCL:
+            if nccl_ids is None or len(nccl_ids) != 2:
+                raise ValueError("tp_size > 1 needs two NCCL unique ids")
+            for lane in range(2):
+                C.memmove(C.addressof(cfg.nccl_id[lane]), bytes(nccl_ids[lane]), 128)
+        self.tp = shard_plan(a, tp_size, tp_rank)
         self.cfg = cfg
         self.handle = C.c_void_p()
         _check(lib().nx_device_create(C.byref(cfg), C.byref(self.handle)))
@@ -140,7 +190,9 @@ class Device:
         b = BatchDesc(lane, sm_pct, n, 0, nt, sp, sa, tk, npg, pg)
         ns = sum(sa)
         out = (C.c_int32 * max(1, ns))()
-        logits = np.zeros((max(1, ns), self.arch.vocab), dtype=np.float32) if want_logits else None
+        local = self.tp.tp_size > 1 and self.cfg.tp_mode == NX_TP_NCCL
+        logits = np.zeros((max(1, ns), self.tp.vocab_local if local else self.arch.vocab),
+                          dtype=np.float32) if want_logits else None
         ms = C.c_double()
         _check(lib().nx_device_forward(self.handle, C.byref(b), out,
                                        logits.ctypes.data_as(C.POINTER(C.c_float)) if want_logits else None,
