@@ -455,13 +455,8 @@ cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                               const AttnSeq* seqs, const int2* work, int n_work,
                               const int32_t* pages, __nv_bfloat16* out, cudaStream_t s) {
   if (n_work == 0) return cudaSuccess;
-  static bool configured = false;
+  ensure_kernels_prepared();
   const size_t smem = attn_smem_bytes_pf();
-  if (!configured) {
-    cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    configured = true;
-  }
   ++g_kernel_launches;
   prefill_attn_kernel<<<dim3(n_work, g.n_kv_heads), kThreadsAttn, smem, s>>>(
       g, qkv, kplane, vplane, seqs, work, pages, out);
@@ -474,13 +469,8 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              __nv_bfloat16* out, float* part_o, float* part_ml, size_t part_cap,
                              int sm_count, cudaStream_t s) {
   if (n_seq == 0) return cudaSuccess;
+  ensure_kernels_prepared();
   const size_t smem = attn_smem_bytes_dec();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    configured = true;
-  }
   const int tiles = (max_kv_len + kKT - 1) / kKT;
   // Enough CTAs for ~2 waves over the partition, at least 2 tiles per split.
   const int base = n_seq * g.n_kv_heads;
@@ -504,6 +494,15 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   decode_combine_kernel<<<dim3(n_seq, g.n_heads), kHD, 0, s>>>(g, seqs, splits, part_o, part_ml,
                                                                out);
   return cudaGetLastError();
+}
+
+void prepare_attention_kernels() {
+  cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(attn_smem_bytes_pf()));
+  cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(attn_smem_bytes_dec()));
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, decode_combine_kernel);
 }
 
 }  // namespace nxd

@@ -13,6 +13,13 @@ namespace nxd {
 // Count of kernels launched by this library (host-side, all streams).
 extern unsigned long long g_kernel_launches;
 
+// Load every kernel and set its shared-memory opt-in on the current device
+// (once per device; see kernels.cu).
+void ensure_kernels_prepared();
+void prepare_gemm_kernels();
+void prepare_attention_kernels();
+void prepare_tp_kernels();
+
 // ---- GEMM (gemm_tc.cu) -------------------------------------------------------
 enum EpiMode {
   kEpiStore = 0,         // out = acc (bf16)

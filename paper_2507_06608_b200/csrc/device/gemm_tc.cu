@@ -547,13 +547,7 @@ template <int BN, int MT>
 cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const GemmParams& p, int grid,
                       cudaStream_t s) {
   using C = Cfg<BN, MT>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, MT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  ensure_kernels_prepared();
   ++g_kernel_launches;
   gemm_tc_kernel<BN, MT><<<grid, kThreads, C::kSmem, s>>>(tw, tx, p);
   return cudaGetLastError();
@@ -670,6 +664,25 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
   ++g_kernel_launches;
   splitk_reduce_kernel<<<(work + 255) / 256, 256, 0, stream>>>(p, mode);
   return cudaGetLastError();
+}
+
+template <int BN, int MT>
+static void prepare_one() {
+  cudaFuncSetAttribute(gemm_tc_kernel<BN, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       Cfg<BN, MT>::kSmem);
+}
+
+void prepare_gemm_kernels() {
+  prepare_one<32, 1>();
+  prepare_one<32, 2>();
+  prepare_one<64, 1>();
+  prepare_one<64, 2>();
+  prepare_one<128, 1>();
+  prepare_one<256, 1>();
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, pack_weights_kernel);
+  cudaFuncGetAttributes(&fa, unpack_weights_kernel);
+  cudaFuncGetAttributes(&fa, splitk_reduce_kernel);
 }
 
 }  // namespace nxd

@@ -2,6 +2,9 @@
 // RoPE + paged KV write, row argmax (greedy sampling), weight init, and the
 // TMA descriptor encoder. All loads/stores are 16-byte vectors.
 #include <cuda_runtime.h>
+
+#include <atomic>
+#include <mutex>
 #include <cudaTypedefs.h>
 
 #include <cfloat>
@@ -331,6 +334,38 @@ bool encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
+}
+
+// Kernel loading is lazy by default (CUDA_MODULE_LOADING=LAZY): the first
+// launch of a kernel loads its module, which can wait for the context to go
+// idle. A TP rank spinning in a peer collective never lets it go idle, so
+// every kernel (and its smem opt-in, which is per device) is prepared up
+// front on each device the library runs on.
+void ensure_kernels_prepared() {
+  static std::atomic<uint64_t> mask{0};
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (mask.load() & bit) return;
+  prepare_gemm_kernels();
+  prepare_attention_kernels();
+  prepare_tp_kernels();
+  const void* fns[] = {reinterpret_cast<const void*>(fill_random_kernel),
+                       reinterpret_cast<const void*>(fill_random_slice_kernel),
+                       reinterpret_cast<const void*>(embed_kernel),
+                       reinterpret_cast<const void*>(rmsnorm_kernel),
+                       reinterpret_cast<const void*>(rope_table_kernel),
+                       reinterpret_cast<const void*>(rope_kv_kernel),
+                       reinterpret_cast<const void*>(argmax_partial_kernel),
+                       reinterpret_cast<const void*>(argmax_final_kernel),
+                       reinterpret_cast<const void*>(argmax_fold_kernel)};
+  cudaFuncAttributes fa;
+  for (const void* f : fns) cudaFuncGetAttributes(&fa, f);
+  cudaGetLastError();
+  mask.fetch_or(bit);
 }
 
 }  // namespace nxd

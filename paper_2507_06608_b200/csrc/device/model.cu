@@ -147,6 +147,7 @@ Model::Model(const nx_device_config& cfg, std::shared_ptr<PeerGroup> group)
   cudaDeviceProp prop{};
   ck(cudaGetDeviceProperties(&prop, cfg.device), "props");
   if (prop.major != 10) throw NoDevice("sm_100 device required");
+  ensure_kernels_prepared();
   parts_.init(cfg.device, cfg.green_contexts != 0);
   tp_ = cfg.tp_size > 1 ? cfg.tp_size : 1;
   rank_ = tp_ > 1 ? cfg.tp_rank : 0;
@@ -169,7 +170,7 @@ Model::Model(const nx_device_config& cfg, std::shared_ptr<PeerGroup> group)
     if (cfg.tp_rank != 0) throw std::invalid_argument("peer TP group is created through rank 0");
     if (cfg.tp_mode == NX_TP_PEER && cfg.device + tp_ > ndev)
       throw NoDevice("NX_TP_PEER needs tp_size GPUs starting at `device`");
-    group_ = std::make_shared<PeerGroup>(tp_);
+    group_ = std::make_shared<PeerGroup>(tp_, cfg.tp_mode == NX_TP_PEER_COLOCATED);
   }
   qkv_rows_ = (hq_ + 2 * hkv_) * a_.head_dim;
   attn_cols_ = hq_ * a_.head_dim;
@@ -217,7 +218,7 @@ Model::Model(const nx_device_config& cfg, std::shared_ptr<PeerGroup> group)
 }
 
 void Model::all_reduce(LaneWs& ws, __nv_bfloat16* x, size_t n) {
-  if (group_) group_->all_reduce_bf16(rank_, ws.slot_index, x, n, ws.stream);
+  if (group_) group_->all_reduce_bf16(rank_, ws.slot_index, x, n, ws.sm_count, ws.stream);
   else Nccl::get().all_reduce_bf16(comm_[ws.slot_index], x, n, ws.stream);
 }
 
@@ -338,6 +339,7 @@ void LaneWs::init(Model* m, int max_tokens) {
   sample_cap = std::min<int>(t_max, 256);
   hs = static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(sample_cap) * a.hidden * 2));
   logits = static_cast<float*>(alloc(static_cast<size_t>(sample_cap) * m->vocab_l_ * 4));
+  out_dev = alloc(T * 4);
   tp_pairs = static_cast<float2*>(alloc(static_cast<size_t>(sample_cap) * (m->tp_ + 1) * sizeof(float2)));
   rope_cs = static_cast<float2*>(alloc(T * (a.head_dim / 2) * sizeof(float2)));
   ws_bytes = 96u << 20;

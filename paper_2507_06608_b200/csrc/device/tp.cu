@@ -209,7 +209,7 @@ __global__ void peer_argmax_kernel(PeerArgs a, const float2* mine_pairs, int32_t
 
 }  // namespace
 
-PeerGroup::PeerGroup(int tp) : tp_(tp) {
+PeerGroup::PeerGroup(int tp, bool colocated) : tp_(tp), colocated_(colocated) {
   if (tp < 2 || tp > kPeerMaxRanks) throw std::invalid_argument("peer TP group size must be 2..8");
   if (cudaHostAlloc(&err_host_, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) !=
       cudaSuccess)
@@ -265,7 +265,8 @@ static PeerArgs make_args(int tp, int rank, uint32_t epoch, int* err, size_t n, 
   return a;
 }
 
-void PeerGroup::all_reduce_bf16(int rank, int lane, __nv_bfloat16* x, size_t n, cudaStream_t s) {
+void PeerGroup::all_reduce_bf16(int rank, int lane, __nv_bfloat16* x, size_t n, int max_ctas,
+                                cudaStream_t s) {
   if (n == 0) return;
   if (n % 8) throw std::invalid_argument("peer all-reduce: n must be a multiple of 8");
   void* bufs[kPeerMaxRanks][2];
@@ -275,7 +276,9 @@ void PeerGroup::all_reduce_bf16(int rank, int lane, __nv_bfloat16* x, size_t n, 
     bufs[r][1] = slot_[r][lane].buf[1];
     flags[r] = slot_[r][lane].flags;
   }
-  const size_t grid = std::min<size_t>(kPeerMaxChunks, std::max<size_t>(1, (n + 8191) / 8192));
+  const size_t cap = static_cast<size_t>(std::max(1, colocated_ ? std::min(max_ctas, 4) : max_ctas));
+  const size_t grid = std::min<size_t>({static_cast<size_t>(kPeerMaxChunks), cap,
+                                        std::max<size_t>(1, (n + 8191) / 8192)});
   const size_t chunk = ((n + grid - 1) / grid + 7) / 8 * 8;
   const uint32_t epoch = ++slot_[rank][lane].epoch;
   PeerArgs a = make_args(tp_, rank, epoch, err_dev_, n, chunk, bufs, flags);
@@ -301,6 +304,12 @@ void PeerGroup::argmax_gather(int rank, int lane, const float2* mine, int n, int
   peer_argmax_kernel<<<1, 256, 0, s>>>(a, mine, out);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("peer argmax: ") + cudaGetErrorString(e));
+}
+
+void prepare_tp_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, peer_allreduce_kernel);
+  cudaFuncGetAttributes(&fa, peer_argmax_kernel);
 }
 
 }  // namespace nxd

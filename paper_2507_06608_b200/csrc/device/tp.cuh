@@ -61,13 +61,16 @@ constexpr int kPeerMaxChunks = 1024;
 
 class PeerGroup {
  public:
-  explicit PeerGroup(int tp);
+  // colocated: every rank on one GPU (tests) — collectives then use a few
+  // CTAs so spinning ranks never starve the ranks they wait for of SMs.
+  PeerGroup(int tp, bool colocated);
   ~PeerGroup();
   // Rank `rank` registers its per-lane exchange buffers (on its own device).
   void register_lane(int rank, int lane, size_t max_elems);
   void release_rank(int rank);
-  // x[0:n) <- sum over ranks of x_r[0:n) (bf16 in, fp32 sum, bf16 out).
-  void all_reduce_bf16(int rank, int lane, __nv_bfloat16* x, size_t n, cudaStream_t s);
+  // x[0:n) <- sum over ranks of x_r[0:n) (bf16 in, fp32 sum, bf16 out), with
+  // at most max_ctas CTAs (the lane's SM count).
+  void all_reduce_bf16(int rank, int lane, __nv_bfloat16* x, size_t n, int max_ctas, cudaStream_t s);
   // tokens[i] <- global argmax from each rank's (max, global idx) pair i.
   void argmax_gather(int rank, int lane, const float2* mine, int n, int32_t* out, cudaStream_t s);
   // Non-zero once a peer wait timed out (a rank never arrived).
@@ -81,6 +84,7 @@ class PeerGroup {
     uint32_t epoch = 0;
   };
   int tp_;
+  bool colocated_;
   Slot slot_[kPeerMaxRanks][2];
   int* err_host_ = nullptr;
   int* err_dev_ = nullptr;

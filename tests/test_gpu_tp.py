@@ -121,7 +121,7 @@ def test_tp_engine_run(nx, pair):
         logs.append(eng.event_log())
         if dev is sharded:
             checked = mism = 0
-            for q in sorted(eng.requests(), key=lambda q: q.prompt_len)[:5]:
+            for q in sorted(eng.requests(), key=lambda q: q.prompt_len)[:10]:
                 toks = eng.tokens(q.id)
                 assert len(toks) == q.prompt_len + q.output_len
                 seq = np.array(toks)
