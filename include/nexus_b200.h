@@ -595,6 +595,9 @@ int nx_dev_sync(void);
  * the epilogue (0 store, 1 bias, 2 residual, 3 bias+residual, 4 SwiGLU,
  * 6 fp32). sm_count caps the persistent grid; splits 0 = automatic.
  * Returns the device time of `iters` launches in *ms (may be NULL). */
+/* Diagnostics: per-CTA %globaltimer milestones of the last GEMM launched with
+ * NX_GEMM_DBG & 16 set ([cta][8] u64); returns the count copied. */
+size_t nx_dbg_gemm_trace(uint64_t* out, size_t n);
 int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32_t K, int32_t mode,
                void* out, int32_t ldo, const void* bias, const void* residual, int32_t ldr,
                int32_t sm_count, int32_t splits, int32_t iters, float* ms);

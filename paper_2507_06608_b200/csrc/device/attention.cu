@@ -34,7 +34,6 @@ constexpr int kKT = 64;         // keys per staged tile
 constexpr int kRowsPF = 64;     // query rows per prefill CTA
 constexpr int kThreadsAttn = 128;
 constexpr int kStagesPF = 2;   // prefill: 2 x 32 KB KV stages (+16 KB Q staging)
-constexpr int kStagesDec = 3;  // decode: 3 x 32 KB in flight per CTA, 2 CTAs / SM
 
 // Swizzled offset (elements) of (row, col) in a [rows][128] bf16 tile.
 __device__ __forceinline__ int swz(int row, int col) {
@@ -290,155 +289,287 @@ __global__ void __launch_bounds__(kThreadsAttn)
   }
 }
 
-// Decode: one token per sequence. 4 warps split every staged 64-key tile
-// into 16-key slices; the warps' (m, l, O) are merged in shared memory.
-__global__ void __launch_bounds__(kThreadsAttn)
+// Decode ("stream-K flash decoding"): the work is the flattened list of
+// 32-key tiles of every (sequence, kv head) item, ordered by sequence then
+// head. Warp w of the persistent grid owns the contiguous tile range
+// [w T / W, (w + 1) T / W) (T tiles, W warps), so every warp streams the same
+// number of KV bytes regardless of the length mix: no wave quantization, no
+// idle tails. Each warp runs its own 3-stage cp.async.bulk ring (one lane
+// issues 2 pages x K/V = 4 x 4 KB copies per tile), continuing across item
+// boundaries so the pipeline never drains. An item covered by one warp is
+// finalized in place; an item split across warps leaves (m, l, O) partials
+// that decode_combine_kernel folds with a log-sum-exp rescale.
+// The G <= 8 query heads of a kv head are the MMA rows (m16n8k16, rows >= G
+// zero); only accumulator rows 0..7 are live, so the softmax touches half of
+// the fragment.
+constexpr int kKTD = 32;      // keys per decode tile (two 16-token pages)
+constexpr int kStD = 3;       // ring stages per warp
+constexpr int kWarpsD = 4;    // warps per CTA (one CTA per SM)
+constexpr int kTileD = kKTD * kHD;  // elements per K (or V) tile
+
+__device__ __forceinline__ void issue_dec_tile(__nv_bfloat16* sk, __nv_bfloat16* sv, uint64_t* bar,
+                                               const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
+                                               const int32_t* pt, int kv_len, int tile, int kvh,
+                                               const AttnGeom& g, uint64_t policy) {
+  const int last_page = pt[(kv_len - 1) >> 4];
+  mbar_expect_tx(bar, 2 * 2 * 4096);
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int key = tile * kKTD + p * 16;
+    const int page = key < kv_len ? pt[key >> 4] : last_page;
+    const size_t off = (static_cast<size_t>(page) * g.n_kv_heads + kvh) * (16 * kHD);
+    bulk_load(sk + p * 16 * kHD, kplane + off, 4096, bar, policy);
+    bulk_load(sv + p * 16 * kHD, vplane + off, 4096, bar, policy);
+  }
+}
+
+// Item (sequence, kv head) holding flattened tile index gt: seq_prefix[s] is
+// the first tile of sequence s (all heads), tiles(s) = ceil(kv_len / 32).
+struct DecPos {
+  int seq, kvh, tile, n_tiles;
+  long long item_start;  // flattened index of the item's first tile
+};
+__device__ __forceinline__ DecPos dec_locate(const int* __restrict__ seq_prefix, int n_seq, int hkv,
+                                             long long gt) {
+  int lo = 0, hi = n_seq - 1;  // last s with seq_prefix[s] * hkv <= gt
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (static_cast<long long>(seq_prefix[mid]) * hkv <= gt) lo = mid;
+    else hi = mid - 1;
+  }
+  DecPos d;
+  d.seq = lo;
+  d.n_tiles = seq_prefix[lo + 1] - seq_prefix[lo];
+  const long long rel = gt - static_cast<long long>(seq_prefix[lo]) * hkv;
+  d.kvh = static_cast<int>(rel / d.n_tiles);
+  d.tile = static_cast<int>(rel % d.n_tiles);
+  d.item_start = static_cast<long long>(seq_prefix[lo]) * hkv + static_cast<long long>(d.kvh) * d.n_tiles;
+  return d;
+}
+
+__device__ __forceinline__ void dec_advance(DecPos& d, const int* __restrict__ seq_prefix, int n_seq,
+                                            int hkv) {
+  if (++d.tile < d.n_tiles) return;
+  d.tile = 0;
+  d.item_start += d.n_tiles;
+  if (++d.kvh == hkv) {
+    d.kvh = 0;
+    if (++d.seq < n_seq) d.n_tiles = seq_prefix[d.seq + 1] - seq_prefix[d.seq];
+  }
+}
+
+__global__ void __launch_bounds__(kWarpsD * 32, 1)
     decode_attn_kernel(AttnGeom g, const __nv_bfloat16* __restrict__ qkv,
                        const __nv_bfloat16* __restrict__ kplane,
                        const __nv_bfloat16* __restrict__ vplane, const AttnSeq* __restrict__ seqs,
-                       const int32_t* __restrict__ pages, int splits, int tiles_per_split,
+                       const int* __restrict__ seq_prefix, int n_seq, long long total, long long W,
+                       const int32_t* __restrict__ pages, int max_pieces,
                        __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
                        float* __restrict__ part_ml) {
   extern __shared__ __align__(1024) uint8_t smem_attn[];
-  constexpr int S = kStagesDec;
-  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_attn);
-  __nv_bfloat16* sv = sk + S * kKT * kHD;
-  __nv_bfloat16* sq = sv + S * kKT * kHD;  // 16 x 128
-  float* red = reinterpret_cast<float*>(sq + 16 * kHD);  // merge scratch
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 128 + 16 * kHD);
-  const int seq = blockIdx.x / splits, split = blockIdx.x % splits;
-  const int kvh = blockIdx.y;
-  const AttnSeq meta = seqs[seq];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t* pt = pages + meta.page_off;
-  const int total_tiles = (meta.kv_len + kKT - 1) / kKT;
-  const int t0 = split * tiles_per_split;
-  const int t1 = min(total_tiles, t0 + tiles_per_split);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+  // per warp: [kStD][K tile][V tile] + Q staging [16][128] + kStD barriers
+  constexpr int kWarpElems = kStD * 2 * kTileD + 16 * kHD;
+  __nv_bfloat16* wbase = reinterpret_cast<__nv_bfloat16*>(smem_attn) + warp * kWarpElems;
+  __nv_bfloat16* sq = wbase + kStD * 2 * kTileD;
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(smem_attn) +
+                                               kWarpsD * kWarpElems) + warp * kStD;
+  // W <= total warps (host), so every range holds >= 1 tile and the warps
+  // covering an item are consecutive: piece = gw - first warp of the item
+  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsD + warp;
+  if (gw >= W) return;
+  const long long lo = total * gw / W, hi = total * (gw + 1) / W;
+  const int hkv = g.n_kv_heads;
+  if (lane == 0) {
+    for (int i = 0; i < kStD; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
-  __syncthreads();
+  __syncwarp();
   const uint64_t pol = policy_evict_first();
-  if (threadIdx.x == 0)
-    for (int t = t0; t < t1 && t < t0 + S; ++t)
-      issue_kv_tile(sk + (t - t0) * kKT * kHD, sv + (t - t0) * kKT * kHD, &full[t - t0], kplane,
-                    vplane, pt, meta.kv_len, t * kKT, kvh, g, pol);
-
-  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-  float o[16][4];
-#pragma unroll
-  for (int d = 0; d < 16; ++d)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) o[d][i] = 0.f;
+  // producer cursor (lane 0) runs kStD tiles ahead of the consumer cursor
+  DecPos prod = dec_locate(seq_prefix, n_seq, hkv, lo);
+  long long issued = lo;
+  if (lane == 0) {
+    for (; issued < hi && issued < lo + kStD; ++issued) {
+      const int st = static_cast<int>(issued - lo);
+      const AttnSeq ms = seqs[prod.seq];
+      issue_dec_tile(wbase + st * 2 * kTileD, wbase + st * 2 * kTileD + kTileD, &full[st], kplane,
+                     vplane, pages + ms.page_off, ms.kv_len, prod.tile, prod.kvh, g, pol);
+      dec_advance(prod, seq_prefix, n_seq, hkv);
+    }
+  }
+  DecPos cur = dec_locate(seq_prefix, n_seq, hkv, lo);
   uint32_t qf[8][4];
-  // every warp loads the same 16-row Q fragment (rows >= G are zero)
-  {
-    for (int c = threadIdx.x; c < 16 * 16; c += kThreadsAttn) {
-      const int r = c >> 4, chunk = c & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < g.group)
-        v = *reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(meta.q_start) * g.qkv_stride +
-                                            (kvh * g.group + r) * kHD + chunk * 8);
-      *reinterpret_cast<uint4*>(sq + r * kHD + ((chunk ^ (r & 7)) << 3)) = v;
-    }
-    __syncthreads();
+  float m = -INFINITY, l = 0.f;  // row lane / 4 (rows 8..15 are padding)
+  float o[16][2];
+  AttnSeq meta = seqs[cur.seq];
+  int seg_tile0 = cur.tile;
+  for (long long gt = lo; gt < hi; ++gt) {
+    const int i = static_cast<int>(gt - lo), buf = i % kStD;
+    if (gt == lo || cur.tile == 0) {  // new segment: this item's queries
+      __syncwarp();
+      meta = seqs[cur.seq];
+      seg_tile0 = cur.tile;
+      for (int c = lane; c < 16 * 16; c += 32) {
+        const int r = c >> 4, chunk = c & 15;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < g.group)
+          v = *reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(meta.q_start) * g.qkv_stride +
+                                              (cur.kvh * g.group + r) * kHD + chunk * 8);
+        *reinterpret_cast<uint4*>(sq + r * kHD + ((chunk ^ (r & 7)) << 3)) = v;
+      }
+      __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int row = (lane & 7) + (((lane >> 3) & 1) << 3);
-      const int col = k * 16 + ((lane >> 4) << 3);
-      ldsm_x4(qf[k], sq + swz(row, col));
-    }
-  }
-  const int lim[2] = {meta.kv_len - 1, meta.kv_len - 1};
-  for (int t = t0; t < t1; ++t) {
-    const int i = t - t0, buf = i % S;
-    mbar_wait(&full[buf], (i / S) & 1);
-    // this warp's 16-key slice; keys past kv_len are masked via the limit
-    attend_tile<true>(qf, sk + buf * kKT * kHD, sv + buf * kKT * kHD, warp * 16, warp * 16 + 16,
-                      lim, m, l, o, g.scale_log2, t * kKT);
-    __syncthreads();
-    if (threadIdx.x == 0 && t + S < t1)
-      issue_kv_tile(sk + buf * kKT * kHD, sv + buf * kKT * kHD, &full[buf], kplane, vplane, pt,
-                    meta.kv_len, (t + S) * kKT, kvh, g, pol);
-  }
-  // merge the 4 warps: rows 0..G-1 live in lanes 0..(4*G-1) (row = lane/4).
+      for (int k = 0; k < 8; ++k) {
+        const int row = (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int col = k * 16 + ((lane >> 4) << 3);
+        ldsm_x4(qf[k], sq + swz(row, col));
+      }
+      m = -INFINITY;
+      l = 0.f;
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    l[r] += __shfl_xor_sync(0xffffffff, l[r], 1);
-    l[r] += __shfl_xor_sync(0xffffffff, l[r], 2);
-  }
-  float* s_m = red;                  // [4 warps][16]
-  float* s_l = red + 64;             // [4][16]
-  float* s_o = red + 128;            // [16 rows][128] accumulated
-  const int row = lane >> 2;
-  if ((lane & 3) == 0) {
-    s_m[warp * 16 + row] = m[0];
-    s_l[warp * 16 + row] = l[0];
-  }
-  for (int i = threadIdx.x; i < 16 * kHD; i += kThreadsAttn) s_o[i] = 0.f;
-  __syncthreads();
-  float M = -INFINITY;
-#pragma unroll
-  for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w * 16 + row]);
-  const float scale_mine = (m[0] == -INFINITY) ? 0.f : exp2f(m[0] - M);
-  if (row < g.group) {
-#pragma unroll
-    for (int d = 0; d < 16; ++d) {
-      const int col = d * 8 + (lane & 3) * 2;
-      atomicAdd(&s_o[row * kHD + col], o[d][0] * scale_mine);
-      atomicAdd(&s_o[row * kHD + col + 1], o[d][1] * scale_mine);
+      for (int d = 0; d < 16; ++d) o[d][0] = o[d][1] = 0.f;
     }
-  }
-  __syncthreads();
-  // finalize: thread -> (row, 8 dims)
-  for (int c = threadIdx.x; c < g.group * 16; c += kThreadsAttn) {
-    const int r = c >> 4, d0 = (c & 15) * 8;
-    float Mr = -INFINITY, L = 0.f;
-    for (int w = 0; w < 4; ++w) Mr = fmaxf(Mr, s_m[w * 16 + r]);
-    for (int w = 0; w < 4; ++w) {
-      const float mw = s_m[w * 16 + r];
-      if (mw != -INFINITY) L += s_l[w * 16 + r] * exp2f(mw - Mr);
+    mbar_wait(&full[buf], (i / kStD) & 1);
+    const __nv_bfloat16* sk = wbase + buf * 2 * kTileD;
+    const __nv_bfloat16* sv = sk + kTileD;
+    // S = Q K^T: 4 blocks of 8 keys, 8 k-steps each (4 independent chains)
+    float s[4][4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int n2 = 0; n2 < 2; ++n2) {
+        uint32_t b[4];
+        const int row = n2 * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int col = k * 16 + (((lane >> 3) & 1) << 3);
+        ldsm_x4(b, sk + swz(row, col));
+        mma16816(s[2 * n2], qf[k], b[0], b[1]);
+        mma16816(s[2 * n2 + 1], qf[k], b[2], b[3]);
+      }
+    // mask keys past kv_len, online softmax on the live row (c0, c1)
+    const int key0 = cur.tile * kKTD;
+    float mx = m;
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int key = key0 + n * 8 + (lane & 3) * 2 + j;
+        s[n][j] = key < meta.kv_len ? s[n][j] * g.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[n][j]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, 2));
+    const float base = mx == -INFINITY ? 0.f : mx;
+    const float alpha = exp2f(m - base);
+    m = mx;
+    l *= alpha;
+#pragma unroll
+    for (int d = 0; d < 16; ++d) o[d][0] *= alpha, o[d][1] *= alpha;
+    uint32_t pf[2][4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const float p0 = exp2f(s[n][0] - base), p1 = exp2f(s[n][1] - base);
+      l += p0 + p1;
+      pf[n >> 1][(n & 1) ? 2 : 0] = pack_bf16(p0, p1);
+      pf[n >> 1][(n & 1) ? 3 : 1] = 0u;  // rows 8..15: padding
     }
-    const int head = kvh * g.group + r;
-    if (splits == 1) {
-      const float inv = L > 0.f ? 1.f / L : 0.f;
-      __align__(16) __nv_bfloat16 v[8];
-      for (int i = 0; i < 8; ++i) v[i] = __float2bfloat16(s_o[r * kHD + d0 + i] * inv);
-      *reinterpret_cast<uint4*>(out + static_cast<size_t>(meta.q_start) * g.out_stride +
-                                head * kHD + d0) = *reinterpret_cast<uint4*>(v);
-    } else {
-      const size_t base = (static_cast<size_t>(seq) * splits + split) * g.n_heads + head;
-      for (int i = 0; i < 8; ++i) part_o[base * kHD + d0 + i] = s_o[r * kHD + d0 + i];
-      if (d0 == 0) {
-        part_ml[base * 2] = Mr;
-        part_ml[base * 2 + 1] = L;
+    // O += P V (16 output blocks of 8 dims, 2 k-steps of 16 keys)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int d2 = 0; d2 < 8; ++d2) {
+        uint32_t b[4];
+        const int row = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int col = d2 * 16 + ((lane >> 4) << 3);
+        ldsm_x4_t(b, sv + swz(row, col));
+        float c0[4] = {o[2 * d2][0], o[2 * d2][1], 0.f, 0.f};
+        float c1[4] = {o[2 * d2 + 1][0], o[2 * d2 + 1][1], 0.f, 0.f};
+        mma16816(c0, pf[ks], b[0], b[1]);
+        mma16816(c1, pf[ks], b[2], b[3]);
+        o[2 * d2][0] = c0[0], o[2 * d2][1] = c0[1];
+        o[2 * d2 + 1][0] = c1[0], o[2 * d2 + 1][1] = c1[1];
+      }
+    __syncwarp();
+    // refill this stage kStD tiles ahead
+    if (lane == 0 && issued < hi) {
+      const AttnSeq ms = seqs[prod.seq];
+      issue_dec_tile(wbase + buf * 2 * kTileD, wbase + buf * 2 * kTileD + kTileD, &full[buf], kplane,
+                     vplane, pages + ms.page_off, ms.kv_len, prod.tile, prod.kvh, g, pol);
+      dec_advance(prod, seq_prefix, n_seq, hkv);
+      ++issued;
+    }
+    // segment end: last tile of the item or of this warp's range
+    const bool item_end = cur.tile == cur.n_tiles - 1;
+    if (item_end || gt == hi - 1) {
+      float lt = l;
+      lt += __shfl_xor_sync(0xffffffff, lt, 1);
+      lt += __shfl_xor_sync(0xffffffff, lt, 2);
+      const int r = lane >> 2;
+      const bool whole = seg_tile0 == 0 && item_end;
+      if (r < g.group) {
+        const int head = cur.kvh * g.group + r;
+        if (whole) {
+          const float inv = lt > 0.f ? 1.f / lt : 0.f;
+          __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + head * kHD;
+#pragma unroll
+          for (int d = 0; d < 16; ++d) {
+            const int col = d * 8 + (lane & 3) * 2;
+            *reinterpret_cast<uint32_t*>(dst + col) = pack_bf16(o[d][0] * inv, o[d][1] * inv);
+          }
+        } else {
+          // piece index of this warp within the item (stream-K ownership rule)
+          const long long first = ((cur.item_start + 1) * W - 1) / total;
+          const size_t slot = (static_cast<size_t>(cur.seq) * hkv + cur.kvh) * max_pieces + (gw - first);
+          float* po = part_o + (slot * g.group + r) * kHD;
+#pragma unroll
+          for (int d = 0; d < 16; ++d) {
+            const int col = d * 8 + (lane & 3) * 2;
+            *reinterpret_cast<float2*>(po + col) = make_float2(o[d][0], o[d][1]);
+          }
+          if ((lane & 3) == 0) {
+            part_ml[(slot * g.group + r) * 2] = m;
+            part_ml[(slot * g.group + r) * 2 + 1] = lt;
+          }
+        }
       }
     }
+    dec_advance(cur, seq_prefix, n_seq, hkv);
   }
 }
 
-// Merge KV-split partials: out = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s.
-__global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ seqs, int splits,
-                                      const float* __restrict__ part_o,
-                                      const float* __restrict__ part_ml,
-                                      __nv_bfloat16* __restrict__ out) {
-  const int seq = blockIdx.x, head = blockIdx.y, d = threadIdx.x;  // 128 threads
+// Folds the pieces of items split across warps:
+// out = sum_p 2^(m_p - M) O_p / sum_p 2^(m_p - M) l_p. CTA = (item, query
+// head), thread = head dim; items covered by a single warp are skipped.
+__global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ seqs,
+                                      const int* __restrict__ seq_prefix, long long total, long long W,
+                                      int max_pieces, const float* __restrict__ part_o,
+                                      const float* __restrict__ part_ml, __nv_bfloat16* __restrict__ out) {
+  const int item = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
+  const int hkv = g.n_kv_heads;
+  const int seq = item / hkv, kvh = item % hkv;
+  const int n_tiles = seq_prefix[seq + 1] - seq_prefix[seq];
+  const long long s0 = static_cast<long long>(seq_prefix[seq]) * hkv + static_cast<long long>(kvh) * n_tiles;
+  const long long first = ((s0 + 1) * W - 1) / total;
+  const long long last = ((s0 + n_tiles) * W - 1) / total;
+  const int pieces = static_cast<int>(last - first + 1);
+  if (pieces <= 1) return;
+  const size_t slot0 = static_cast<size_t>(item) * max_pieces * g.group + r;
   float M = -INFINITY;
-  for (int s = 0; s < splits; ++s)
-    M = fmaxf(M, part_ml[((static_cast<size_t>(seq) * splits + s) * g.n_heads + head) * 2]);
+  for (int q = 0; q < pieces; ++q) M = fmaxf(M, part_ml[(slot0 + static_cast<size_t>(q) * g.group) * 2]);
   float acc = 0.f, L = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const size_t base = (static_cast<size_t>(seq) * splits + s) * g.n_heads + head;
-    const float ms = part_ml[base * 2];
-    if (ms == -INFINITY) continue;
-    const float w = exp2f(ms - M);
-    L += part_ml[base * 2 + 1] * w;
-    acc += part_o[base * kHD + d] * w;
+  for (int q = 0; q < pieces; ++q) {
+    const size_t slot = slot0 + static_cast<size_t>(q) * g.group;
+    const float ms = part_ml[slot * 2];
+    const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+    L += part_ml[slot * 2 + 1] * w;
+    acc += part_o[slot * kHD + d] * w;
   }
-  out[static_cast<size_t>(seqs[seq].q_start) * g.out_stride + head * kHD + d] =
+  out[static_cast<size_t>(seqs[seq].q_start) * g.out_stride + (kvh * g.group + r) * kHD + d] =
       __float2bfloat16(L > 0.f ? acc / L : 0.f);
 }
+
 
 }  // namespace
 
@@ -446,7 +577,7 @@ size_t attn_smem_bytes_pf() {
   return static_cast<size_t>(2 * kStagesPF * kKT * kHD + 4 * 16 * kHD) * 2 + 64;
 }
 size_t attn_smem_bytes_dec() {
-  return static_cast<size_t>(2 * kStagesDec * kKT * kHD + 16 * kHD) * 2 + (128 + 16 * kHD) * 4 + 64;
+  return static_cast<size_t>(kWarpsD) * (kStD * 2 * kTileD + 16 * kHD) * 2 + kWarpsD * kStD * 8 + 64;
 }
 size_t attn_smem_bytes() { return std::max(attn_smem_bytes_pf(), attn_smem_bytes_dec()); }
 
@@ -465,34 +596,30 @@ cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
 
 cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
-                             const AttnSeq* seqs, int n_seq, int max_kv_len, const int32_t* pages,
+                             const AttnSeq* seqs, int n_seq, const int* seq_prefix,
+                             long long total_tiles, int max_seq_tiles, const int32_t* pages,
                              __nv_bfloat16* out, float* part_o, float* part_ml, size_t part_cap,
                              int sm_count, cudaStream_t s) {
-  if (n_seq == 0) return cudaSuccess;
+  if (n_seq == 0 || total_tiles == 0) return cudaSuccess;
+  if (g.group > 8) return cudaErrorInvalidValue;
   ensure_kernels_prepared();
   const size_t smem = attn_smem_bytes_dec();
-  const int tiles = (max_kv_len + kKT - 1) / kKT;
-  // Enough CTAs for ~2 waves over the partition, at least 2 tiles per split.
-  const int base = n_seq * g.n_kv_heads;
-  int splits = 1;
-  if (part_o != nullptr && base < 2 * sm_count) {
-    splits = (2 * sm_count + base - 1) / base;
-    splits = std::min(splits, std::max(1, tiles / 2));
-    splits = std::min(splits, 32);
-    while (splits > 1 &&
-           static_cast<size_t>(n_seq) * splits * g.n_heads * kHD > part_cap)
-      --splits;
-  }
-  const int per = (tiles + splits - 1) / splits;
-  splits = std::max(1, (tiles + per - 1) / per);
+  const long long W = std::min<long long>(static_cast<long long>(sm_count) * kWarpsD, total_tiles);
+  const int grid = static_cast<int>((W + kWarpsD - 1) / kWarpsD);
+  // pieces per item <= ceil(tiles / min range) + 1
+  const long long per_min = std::max<long long>(1, total_tiles / W);
+  const int max_pieces = static_cast<int>((max_seq_tiles + per_min - 1) / per_min) + 1;
+  if (static_cast<size_t>(n_seq) * g.n_kv_heads * max_pieces * g.group * kHD > part_cap)
+    return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  decode_attn_kernel<<<dim3(n_seq * splits, g.n_kv_heads), kThreadsAttn, smem, s>>>(
-      g, qkv, kplane, vplane, seqs, pages, splits, per, out, part_o, part_ml);
+  decode_attn_kernel<<<grid, kWarpsD * 32, smem, s>>>(g, qkv, kplane, vplane, seqs, seq_prefix, n_seq,
+                                                      total_tiles, W, pages, max_pieces, out, part_o,
+                                                      part_ml);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || splits == 1) return e;
+  if (e != cudaSuccess) return e;
   ++g_kernel_launches;
-  decode_combine_kernel<<<dim3(n_seq, g.n_heads), kHD, 0, s>>>(g, seqs, splits, part_o, part_ml,
-                                                               out);
+  decode_combine_kernel<<<dim3(n_seq * g.n_kv_heads, g.group), kHD, 0, s>>>(g, seqs, seq_prefix, total_tiles, W, max_pieces,
+                                                            part_o, part_ml, out);
   return cudaGetLastError();
 }
 

@@ -180,6 +180,10 @@ int nx_dev_d2h(void* dst, const void* src, size_t n) {
 }
 int nx_dev_sync(void) { return cuda_rc(cudaDeviceSynchronize()); }
 
+size_t nx_dbg_gemm_trace(uint64_t* out, size_t n) {
+  return nxd::gemm_trace_read(reinterpret_cast<unsigned long long*>(out), n);
+}
+
 int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32_t K, int32_t mode,
                void* out, int32_t ldo, const void* bias, const void* residual, int32_t ldr,
                int32_t sm_count, int32_t splits, int32_t iters, float* ms) {
@@ -218,7 +222,7 @@ int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32
       err = nxd::gemm(wp, xm, bn, rows, tokens, K, mode, out, ldo,
                       static_cast<const __nv_bfloat16*>(bias),
                       static_cast<const __nv_bfloat16*>(residual), ldr, ws, ws_bytes, sm_count,
-                      nullptr, splits);
+                      nullptr, splits, /*coresident=*/true);
       cudaEventRecord(ev[2 * i + 1], nullptr);
     }
     if (err == cudaSuccess) err = cudaDeviceSynchronize();

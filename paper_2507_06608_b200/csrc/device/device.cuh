@@ -46,9 +46,13 @@ struct GemmParams {
   int bn;          // token tile (for the stream-K fix-up)
   int* tile_count; // stream-K: per-tile arrival counters (zero between launches)
   int n_tiles128;  // 128-row weight blocks (n_mblk counts MT-block work tiles)
+  int coresident;  // stream-K: parallel reduce-scatter fix-up (see gemm())
+  int dbg;         // experiments only (NX_GEMM_DBG): 1 skip X loads, 2 skip MMAs
 };
 
 int gemm_pick_bn(int tokens);
+// Experiments: copies the per-CTA milestone stamps (NX_GEMM_DBG & 16).
+size_t gemm_trace_read(unsigned long long* host, size_t n);
 // y[tokens, rows] = epi(x[tokens, K] . w[rows, K]^T). `x_map` must have been
 // encoded with box rows == bn. sm_count sizes the persistent grid (the lane's
 // green-context partition); force_splits > 0 overrides the K-split choice.
@@ -64,8 +68,13 @@ cudaError_t unpack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int row
 cudaError_t gemm(const __nv_bfloat16* w_packed, const CUtensorMap& x_map, int bn, int rows, int tokens,
                  int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
                  const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
-                 cudaStream_t stream, int force_splits = 0);
+                 cudaStream_t stream, int force_splits = 0, bool coresident = false);
+// coresident: the launch owns its SMs (green-context partition, or nothing
+// else running), so every CTA of the persistent grid is resident at once and
+// stream-K pieces may wait for each other (parallel fix-up); otherwise the
+// last arriving piece folds the tile alone.
 constexpr size_t gemm_counter_bytes() { return 64 * 1024; }
+constexpr int kGemmMaxCounterTiles = 8192;  // [arrive | depart] int counters
 
 // K-major bf16 [rows, cols] tensor map with a 64 x box_rows, 128B-swizzled box.
 bool encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
@@ -93,9 +102,14 @@ cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                               const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
                               const AttnSeq* seqs, const int2* work, int n_work,
                               const int32_t* pages, __nv_bfloat16* out, cudaStream_t s);
+// Decode attention over 32-key tiles (kDecTileKeys): seq_prefix[s] = first
+// tile of sequence s, sum_{s' < s} ceil(kv_len(s') / 32) (n_seq + 1 entries,
+// device memory); total_tiles = seq_prefix[n_seq] * n_kv_heads.
+constexpr int kDecTileKeys = 32;
 cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
-                             const AttnSeq* seqs, int n_seq, int max_kv_len, const int32_t* pages,
+                             const AttnSeq* seqs, int n_seq, const int* seq_prefix,
+                             long long total_tiles, int max_seq_tiles, const int32_t* pages,
                              __nv_bfloat16* out, float* part_o, float* part_ml, size_t part_cap,
                              int sm_count, cudaStream_t s);
 

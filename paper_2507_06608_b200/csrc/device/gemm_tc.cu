@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "ptx.cuh"
@@ -54,6 +55,16 @@ struct Cfg {
   static_assert(kStages >= 2, "pipeline too shallow");
   static_assert(2 * MT * BN <= 512, "TMEM: 512 columns");
 };
+
+// Experiments only (NX_GEMM_DBG & 16): per-CTA %globaltimer stamps of the
+// pipeline milestones, read back with nx_dbg_gemm_trace.
+__device__ unsigned long long g_gemm_trace[1024][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define NX_STAMP(i) do { if (p.dbg & 16) g_gemm_trace[blockIdx.x & 1023][i] = gtimer(); } while (0)
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
@@ -264,6 +275,138 @@ __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& 
   }
 }
 
+// Stream-K fix-up when all CTAs are co-resident (p.coresident): every piece
+// publishes its fp32 partial and counts itself in; once a tile's pieces are
+// all in, piece i folds rows [i R/P, (i+1) R/P) of the tile (R = tokens x
+// sub-tiles) across all P partials and applies the epilogue. The fold is
+// spread over the P CTAs instead of serialized on the last arriver, and its
+// loads are issued P-deep. The last piece to leave resets the counters.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void streamk_tile_pieces(const GemmParams& p, int tile, int* first, int* pieces) {
+  const long long total = static_cast<long long>(p.n_mblk) * p.n_nblk * p.num_kb;
+  const long long it0 = static_cast<long long>(tile) * p.num_kb;
+  *first = static_cast<int>(((it0 + 1) * gridDim.x - 1) / total);
+  const int last = static_cast<int>(((it0 + p.num_kb) * gridDim.x - 1) / total);
+  *pieces = last - *first + 1;
+}
+
+__device__ __forceinline__ void store_out4(const GemmParams& p, int t, int f, float4 a) {
+  if (p.mode == kEpiF32) {
+    *reinterpret_cast<float4*>(static_cast<float*>(p.out) + static_cast<size_t>(t) * p.ldo + f) = a;
+    return;
+  }
+  if (p.mode == kEpiBias || p.mode == kEpiBiasResidual) {
+    const __nv_bfloat162 b01 = *reinterpret_cast<const __nv_bfloat162*>(p.bias + f);
+    const __nv_bfloat162 b23 = *reinterpret_cast<const __nv_bfloat162*>(p.bias + f + 2);
+    a.x += __low2float(b01), a.y += __high2float(b01), a.z += __low2float(b23), a.w += __high2float(b23);
+  }
+  if (p.mode == kEpiResidual || p.mode == kEpiBiasResidual) {
+    const __nv_bfloat16* rp = p.residual + static_cast<size_t>(t) * p.ldr + f;
+    const __nv_bfloat162 r01 = *reinterpret_cast<const __nv_bfloat162*>(rp);
+    const __nv_bfloat162 r23 = *reinterpret_cast<const __nv_bfloat162*>(rp + 2);
+    a.x += __low2float(r01), a.y += __high2float(r01), a.z += __low2float(r23), a.w += __high2float(r23);
+  }
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo + f;
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+  uint2 v;
+  v.x = *reinterpret_cast<uint32_t*>(&lo);
+  v.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst) = v;
+}
+
+template <int BN, int MT>
+__device__ void streamk_publish(const GemmParams& p, const Work& w, int et) {
+  __threadfence();
+  named_bar_sync(1, kEpiThreads);
+  if (et == 0) atomicAdd(&p.tile_count[w.m_blk * p.n_nblk + w.n_blk], 1);
+}
+
+template <int BN, int MT>
+__device__ void streamk_reduce_slice(const GemmParams& p, int m_blk, int n_blk, int et, uint8_t* scratch,
+                                     uint64_t* bar, uint32_t& phase) {
+  const int tile = m_blk * p.n_nblk + n_blk;
+  int first, pieces;
+  streamk_tile_pieces(p, tile, &first, &pieces);
+  const int piece = static_cast<int>(blockIdx.x) - first;
+  int* arrive = p.tile_count + tile;
+  int* depart = p.tile_count + kGemmMaxCounterTiles + tile;
+  const int tok_base = n_blk * BN;
+  const int n_tok = min(BN, p.tokens - tok_base);
+  const int valid = min(MT, p.n_tiles128 - m_blk * MT);
+  const int R = valid * n_tok;
+  const int r0 = R * piece / pieces, r1 = R * (piece + 1) / pieces;
+  const int nrows = r1 - r0;
+  constexpr int kRowBytes = kBM * 4;
+  if (et == 0) {
+    while (ld_acquire_gpu(arrive) < pieces) __nanosleep(32);
+    // one bulk copy per (piece, sub-tile run of rows): the whole slice of
+    // every partial lands in shared memory after a single round trip
+    if (nrows > 0) {
+      mbar_expect_tx(bar, static_cast<uint32_t>(pieces * nrows * kRowBytes));
+      const float* base = p.ws + static_cast<size_t>(tile) * p.max_pieces * MT * BN * kBM;
+      for (int q = 0; q < pieces; ++q) {
+        int r = r0;
+        while (r < r1) {
+          const int sub = r / n_tok, j = r % n_tok;
+          const int run = min(r1 - r, n_tok - j);
+          const float* src = base + ((static_cast<size_t>(q) * MT + sub) * BN + j) * kBM;
+          bulk_load(scratch + (static_cast<size_t>(q) * nrows + (r - r0)) * kRowBytes, src,
+                    static_cast<uint32_t>(run * kRowBytes), bar);
+          r += run;
+        }
+      }
+    }
+  }
+  named_bar_sync(1, kEpiThreads);
+  if (nrows > 0) {
+    mbar_wait(bar, phase);
+    phase ^= 1;
+  }
+  const bool swiglu = p.mode == kEpiSwiGLU;
+  const int per_row = swiglu ? 16 : 32;  // float4 units per (sub, token) row
+  const int units = nrows * per_row;
+  const float4* sc = reinterpret_cast<const float4*>(scratch);
+  const int slice4 = nrows * (kBM / 4);
+  for (int u = et; u < units; u += kEpiThreads) {
+    const int lr = u / per_row, c4 = u % per_row;
+    const int pos = lr * (kBM / 4) + c4;
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f), up = g;
+    for (int q = 0; q < pieces; ++q) {
+      const float4 v = sc[q * slice4 + pos];
+      g.x += v.x, g.y += v.y, g.z += v.z, g.w += v.w;
+      if (swiglu) {
+        const float4 b = sc[q * slice4 + pos + 16];
+        up.x += b.x, up.y += b.y, up.z += b.z, up.w += b.w;
+      }
+    }
+    const int row = r0 + lr;
+    const int sub = row / n_tok, j = row % n_tok, c = c4 * 4;
+    const int t = tok_base + j;
+    const int m128 = m_blk * MT + sub;
+    if (swiglu) {
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo + m128 * 64 + c;
+      __nv_bfloat162 lo = __floats2bfloat162_rn(silu(g.x) * up.x, silu(g.y) * up.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(silu(g.z) * up.z, silu(g.w) * up.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&lo);
+      o.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(dst) = o;
+    } else {
+      store_out4(p, t, m128 * kBM + c, g);
+    }
+  }
+  named_bar_sync(1, kEpiThreads);
+  if (et == 0 && atomicAdd(depart, 1) == pieces - 1) {
+    *arrive = 0;  // every piece is past its wait: ready for the next launch
+    *depart = 0;
+  }
+}
+
 template <int BN, int MT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __nv_bfloat16* __restrict__ wpack, const __grid_constant__ CUtensorMap tx,
@@ -277,10 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* fix_bar = tempty + 2;  // parallel stream-K fix-up loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) NX_STAMP(0);
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tx);
     for (int s = 0; s < C::kStages; ++s) {
@@ -291,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiThreads);
     }
+    mbar_init(fix_bar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -298,6 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) NX_STAMP(1);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -312,18 +459,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStage;
-          mbar_expect_tx(&full[stage], valid * kABytes + C::kBBytes);
+          mbar_expect_tx(&full[stage], valid * kABytes + ((p.dbg & 1) ? 0 : C::kBBytes));
           // weight tiles = contiguous pre-swizzled 16 KB chunks (pack_weights); an
           // aligned pair of row blocks is one 32 KB copy
           if (MT == 2 && valid == 2) {
             bulk_load(sa, wpack + packed_tile_offset(w.m_blk * 2, kb, p.num_kb), 2 * kABytes,
                       &full[stage], w_policy);
           } else {
-            for (int t = 0; t < valid; ++t)
-              bulk_load(sa + t * kABytes, wpack + packed_tile_offset(w.m_blk * MT + t, kb, p.num_kb),
-                        kABytes, &full[stage], w_policy);
+            for (int t = 0; t < valid; ++t) {
+              const size_t off = (p.dbg & 4)
+                  ? (static_cast<size_t>(w.m_blk * MT + t) * p.num_kb + kb) * (kBM * kBK)
+                  : packed_tile_offset(w.m_blk * MT + t, kb, p.num_kb);
+              if (p.dbg & 8)
+                bulk_load(sa + t * kABytes, wpack + off, kABytes, &full[stage]);
+              else
+                bulk_load(sa + t * kABytes, wpack + off, kABytes, &full[stage], w_policy);
+            }
           }
-          tma_load_2d(&tx, &full[stage], sa + MT * kABytes, kb * kBK, w.n_blk * BN);
+          if (!(p.dbg & 1)) tma_load_2d(&tx, &full[stage], sa + MT * kABytes, kb * kBK, w.n_blk * BN);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -348,11 +501,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
+        if (local == 0 && kb == kb0 && lane_id() == 0) NX_STAMP(2);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t base = smem_u32(smem + stage * C::kStage);
           const uint32_t b_addr = base + MT * kABytes;
-          for (int t = 0; t < valid; ++t) {
+          for (int t = 0; t < ((p.dbg & 2) ? 0 : valid); ++t) {
             const uint32_t d = tmem + (acc * MT + t) * BN;
             const uint32_t a_addr = base + t * kABytes;
 #pragma unroll
@@ -362,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           umma_commit(&empty[stage]);
           if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+          NX_STAMP(3);
         }
         __syncwarp();
         if (++stage == C::kStages) {
@@ -376,12 +531,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int et = threadIdx.x - 64;
     const int lane = lane_id();
     int local = 0;
+    int pend_m[2], pend_n[2], n_pend = 0;  // partial items awaiting the parallel fix-up
     WorkIter wi(p);
     Work w;
     for (; wi.next(w); ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
+      if (et == 0) NX_STAMP(4);
       tc_fence_after();
       const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
       for (int sub = 0; sub < valid; ++sub)
@@ -480,10 +637,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (p.streamk && w.partial) streamk_arrive<BN, MT>(p, w, et, s_flag);
+      if (et == 0) NX_STAMP(5);
+      if (p.streamk && w.partial) {
+        if (p.coresident && n_pend < 2) {
+          // publish now, fold after the last item: publishing never waits,
+          // so no chain of waits can form across CTAs
+          streamk_publish<BN, MT>(p, w, et);
+          pend_m[n_pend] = w.m_blk;
+          pend_n[n_pend++] = w.n_blk;
+        } else {
+          streamk_arrive<BN, MT>(p, w, et, s_flag);
+        }
+      }
     }
+    // the stage ring is idle now (every stage was consumed by the MMAs that
+    // produced the accumulators above): it stages the fix-up slices
+    uint32_t fix_phase = 0;
+    for (int i = 0; i < n_pend; ++i)
+      streamk_reduce_slice<BN, MT>(p, pend_m[i], pend_n[i], et, smem, fix_bar, fix_phase);
+    if (et == 0) NX_STAMP(6);
   }
   __syncthreads();
+  if (threadIdx.x == 0) NX_STAMP(7);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
@@ -584,7 +759,7 @@ int gemm_pick_bn(int tokens) {
 cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, int bn, int rows,
                  int tokens, int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
                  const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
-                 cudaStream_t stream, int force_splits) {
+                 cudaStream_t stream, int force_splits, bool coresident) {
   if (tokens <= 0) return cudaSuccess;
   if (rows % kBM || K % kBK) return cudaErrorInvalidValue;
   GemmParams p{};
@@ -607,6 +782,12 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
   p.residual = residual;
   p.ldr = ldr;
   p.bn = bn;
+  static const int dbg = [] {
+    const char* e = std::getenv("NX_GEMM_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.dbg = dbg;
+  p.coresident = coresident ? 1 : 0;
   // ws layout: [int tile counters | fp32 partials]
   p.tile_count = reinterpret_cast<int*>(ws);
   p.ws = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + gemm_counter_bytes()) : nullptr;
@@ -631,7 +812,7 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
     p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
     grid = std::max(1, std::min(tiles * p.splits, sm_count));
   } else if (tokens <= 256 && ws != nullptr && tiles % sm_count != 0 &&
-             static_cast<size_t>(tiles) * 4 <= gemm_counter_bytes()) {
+             tiles <= kGemmMaxCounterTiles) {
     // Stream-K: equal (tile, k-block) ranges per CTA remove the wave tail
     // of decode-shaped launches (weight streaming: every CTA busy to the end).
     const int G = static_cast<int>(std::min<long long>(sm_count, iters));
@@ -683,6 +864,13 @@ void prepare_gemm_kernels() {
   cudaFuncGetAttributes(&fa, pack_weights_kernel);
   cudaFuncGetAttributes(&fa, unpack_weights_kernel);
   cudaFuncGetAttributes(&fa, splitk_reduce_kernel);
+}
+
+size_t gemm_trace_read(unsigned long long* host, size_t n) {
+  const size_t cap = sizeof(g_gemm_trace) / sizeof(unsigned long long);
+  if (n > cap) n = cap;
+  if (cudaMemcpyFromSymbol(host, g_gemm_trace, n * sizeof(unsigned long long)) != cudaSuccess) return 0;
+  return n;
 }
 
 }  // namespace nxd

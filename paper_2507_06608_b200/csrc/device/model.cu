@@ -94,6 +94,7 @@ Partitions::Pick Partitions::pick(int lane_kind, int sm_pct) const {
                                                                : plain_stream[lane_kind == 2 ? 1 : 0];
     p.sm_count = total_sm;
     p.layout = -1;
+    p.exclusive = enabled || lane_kind == 3;
     return p;
   }
   const double target = sm_pct / 100.0 * total_sm;
@@ -111,6 +112,7 @@ Partitions::Pick Partitions::pick(int lane_kind, int sm_pct) const {
   p.stream = lane_kind == 2 ? l.decode_stream : l.prefill_stream;
   p.sm_count = lane_kind == 2 ? l.decode_sms : l.prefill_sms;
   p.layout = best;
+  p.exclusive = true;
   return p;
 }
 
@@ -392,6 +394,7 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   ws.stream = pk.stream;
   ws.sm_count = pk.sm_count;
   ws.layout = pk.layout;
+  ws.exclusive = pk.exclusive;
   // ---- pack metadata into the pinned mirror ----
   int T = 0, n_sample = 0, n_pages_total = 0;
   for (const auto& m : b.members) {
@@ -413,6 +416,7 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   const size_t o_seq = carve(n_seq * sizeof(AttnSeq));
   const size_t o_pages = carve(n_pages_total * 4 + 4);
   const size_t o_rows = carve(n_sample * 4 + 4);
+  const size_t o_dpre = carve((n_seq + 1) * 4);
   int max_work = 0;
   for (const auto& m : b.members)
     max_work += (m.n_tokens * (hq_ / hkv_) + 63) / 64;
@@ -424,10 +428,12 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   int32_t* pages = reinterpret_cast<int32_t*>(hp + o_pages);
   int32_t* rows = reinterpret_cast<int32_t*>(hp + o_rows);
   int2* work = reinterpret_cast<int2*>(hp + o_work);
+  int32_t* dpre = reinterpret_cast<int32_t*>(hp + o_dpre);
   const int group = hq_ / hkv_;
   int t = 0, pg = 0, ns = 0, nw = 0;
   ws.dec_seq_count = 0;
   ws.max_dec_kv = 0;
+  ws.max_dec_tiles = 0;
   ws.dec_kv_tokens = ws.pre_kv_tokens = ws.pre_pairs = 0;
   ws.is_decode_lane = slot == nxb::kLaneDecode;
   // decode members (q_len == 1) first in the seq table so the decode kernel
@@ -449,6 +455,10 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
     if (m.sample) rows[ns++] = t + m.n_tokens - 1;
     if (!m.is_prefill) {
       if (i != ws.dec_seq_count) throw std::runtime_error("decode members must come first");
+      const int tiles = (s.kv_len + kDecTileKeys - 1) / kDecTileKeys;
+      if (i == 0) dpre[0] = 0;
+      dpre[i + 1] = dpre[i] + tiles;
+      ws.max_dec_tiles = std::max(ws.max_dec_tiles, tiles);
       ws.dec_seq_count++;
       ws.max_dec_kv = std::max(ws.max_dec_kv, s.kv_len);
       ws.dec_kv_tokens += s.kv_len;
@@ -479,6 +489,8 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   ws.d_pages = reinterpret_cast<const int32_t*>(dp + o_pages);
   ws.d_rows = reinterpret_cast<const int32_t*>(dp + o_rows);
   ws.d_work = reinterpret_cast<const int2*>(dp + o_work);
+  ws.d_dec_prefix = reinterpret_cast<const int32_t*>(dp + o_dpre);
+  ws.dec_total_tiles = ws.dec_seq_count ? static_cast<long long>(dpre[ws.dec_seq_count]) * hkv_ : 0;
   forward(ws);
   ck(cudaMemcpyAsync(ws.out_host, ws.d_out_tokens, static_cast<size_t>(ns) * 4,
                      cudaMemcpyDeviceToHost, s),
@@ -538,7 +550,7 @@ void Model::forward(LaneWs& ws) {
     });
     timed(gk, gbytes(qkv_rows_, d, 2, false), gflops(qkv_rows_, d), [&] {
       ck(gemm(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
-              ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+              ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "qkv gemm");
     });
     timed(NX_K_OTHER, Td * qkv_rows_ * 4, 0, [&] {
@@ -550,8 +562,8 @@ void Model::forward(LaneWs& ws) {
       timed(NX_K_ATTN_DECODE, ws.dec_kv_tokens * kvtok + ws.dec_seq_count * qo,
             4.0 * ws.dec_kv_tokens * attn_cols_, [&] {
               ck(decode_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.dec_seq_count,
-                                  ws.max_dec_kv, ws.d_pages, ws.attn, ws.part_o, ws.part_ml,
-                                  ws.part_cap, sm, s),
+                                  ws.d_dec_prefix, ws.dec_total_tiles, ws.max_dec_tiles, ws.d_pages,
+                                  ws.attn, ws.part_o, ws.part_ml, ws.part_cap, sm, s),
                  "decode attention");
             });
     if (ws.n_work > 0)
@@ -566,7 +578,7 @@ void Model::forward(LaneWs& ws) {
     const int res_mode = (tp_ == 1 || rank_ == 0) ? kEpiResidual : kEpiStore;
     timed(gk, gbytes(d, attn_cols_, 2, true), gflops(d, attn_cols_), [&] {
       ck(gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x,
-              d, ws.ws, ws.ws_bytes, sm, s),
+              d, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "o gemm");
     });
     if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
@@ -575,12 +587,12 @@ void Model::forward(LaneWs& ws) {
     });
     timed(gk, gbytes(2.0 * ffn_, d, 1, false), gflops(2.0 * ffn_, d), [&] {
       ck(gemm(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr,
-              nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+              nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "gate/up gemm");
     });
     timed(gk, gbytes(d, ffn_, 2, true), gflops(d, ffn_), [&] {
       ck(gemm(w.down, ws.map_act[bi], bn, d, T, ffn_, res_mode, ws.x, d, nullptr, ws.x, d,
-              ws.ws, ws.ws_bytes, sm, s),
+              ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "down gemm");
     });
     if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
@@ -597,7 +609,7 @@ void Model::forward(LaneWs& ws) {
     timed(gk, static_cast<double>(vocab_l_) * d * 2 + nd * d * 2 + nd * vocab_l_ * 4,
           2.0 * nd * vocab_l_ * d, [&] {
             ck(gemm(lm_head_, ws.map_hs[bn_index(sbn)], sbn, vocab_l_, n, d, kEpiF32, ws.logits,
-                    vocab_l_, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s),
+                    vocab_l_, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
                "lm_head gemm");
           });
     timed(NX_K_OTHER, nd * vocab_l_ * 4, 0, [&] {

@@ -31,6 +31,7 @@ struct Partitions {
     cudaStream_t stream = nullptr;
     int sm_count = 0;
     int layout = -1;
+    bool exclusive = false;  // the stream owns its SMs (green partition / whole GPU)
   };
   void init(int device, bool enable);
   Pick pick(int lane_kind, int sm_pct) const;
@@ -71,7 +72,11 @@ struct LaneWs {
   // current batch
   cudaStream_t stream = nullptr;
   int sm_count = 0, layout = -1;
+  bool exclusive = false;
   int tokens = 0, n_seq = 0, n_work = 0, n_sample = 0, dec_seq_count = 0, max_dec_kv = 0;
+  int max_dec_tiles = 0;
+  long long dec_total_tiles = 0;
+  const int32_t* d_dec_prefix = nullptr;
   const int32_t *d_tok = nullptr, *d_pos = nullptr, *d_slot = nullptr, *d_pages = nullptr,
                 *d_rows = nullptr;
   const AttnSeq* d_seqs = nullptr;

@@ -118,3 +118,22 @@ def test_long_context_decode_splits(gqa):
     out, logits, _ = dev.forward([dict(tokens=[seq[-1]], start=len(seq) - 1, pages=pages)], lane=1,
                                  sm_pct=10, want_logits=True)
     _check_logits(logits, ref.logits(np.array(seq))[-1:], out)
+
+
+@pytest.mark.parametrize("ctx", [40, 600, 5000])
+def test_decode_long_context_all_partitions(tiny, ctx):
+    """Decode attention distributes the flattened 32-key tiles of all
+    (sequence, kv head) items over the warps of the lane's partition; a
+    context is split across 1..hundreds of warps depending on the partition
+    size, and the pieces are folded by the combine kernel. Same logits at
+    every partition size, against the fp32 oracle."""
+    dev, ref = tiny
+    rng = np.random.default_rng(ctx)
+    prompt = rng.integers(0, dev.arch.vocab, ctx).tolist()
+    pages = [int(p) for p in rng.permutation(2000)[:ctx // 16 + 4]]
+    for c0 in range(0, ctx, 2048):
+        dev.forward([dict(tokens=prompt[c0:c0 + 2048], start=c0, pages=pages, sample=False)], lane=0, sm_pct=60)
+    want = ref.logits(np.array(prompt + [5]))[-1:]
+    for pct in (5, 30, 99):
+        out, lg, _ = dev.forward([dict(tokens=[5], start=ctx, pages=pages)], lane=1, sm_pct=pct, want_logits=True)
+        _check_logits(lg, want, out)
