@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kThreadsAttn)
   __nv_bfloat16* sv = sk + S * kKT * kHD;                            // [S][64][128]
   __nv_bfloat16* sq = sv + S * kKT * kHD;                            // [4 warps][16][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sq + 4 * 16 * kHD);
+  pdl_trigger();
   const int2 wi = work[blockIdx.x];
   const AttnSeq sq_meta = seqs[wi.x];
   const int kvh = blockIdx.y;
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(kThreadsAttn)
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();  // K/V of this chunk and Q come from the QKV / RoPE kernels
   const uint64_t pol = policy_evict_first();
   if (threadIdx.x == 0)
     for (int t = 0; t < S && t < n_tiles; ++t)
@@ -376,6 +378,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
                                                kWarpsD * kWarpElems) + warp * kStD;
   // W <= total warps (host), so every range holds >= 1 tile and the warps
   // covering an item are consecutive: piece = gw - first warp of the item
+  pdl_trigger();
   const long long gw = static_cast<long long>(blockIdx.x) * kWarpsD + warp;
   if (gw >= W) return;
   const long long lo = total * gw / W, hi = total * (gw + 1) / W;
@@ -385,6 +388,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
     fence_barrier_init();
   }
   __syncwarp();
+  pdl_wait();  // the new token's K/V and Q come from the QKV / RoPE kernels
   const uint64_t pol = policy_evict_first();
   // producer cursor (lane 0) runs kStD tiles ahead of the consumer cursor
   DecPos prod = dec_locate(seq_prefix, n_seq, hkv, lo);
@@ -546,6 +550,8 @@ __global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ se
                                       const int* __restrict__ seq_prefix, long long total, long long W,
                                       int max_pieces, const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int item = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
   const int hkv = g.n_kv_heads;
   const int seq = item / hkv, kvh = item % hkv;
@@ -589,9 +595,8 @@ cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   ensure_kernels_prepared();
   const size_t smem = attn_smem_bytes_pf();
   ++g_kernel_launches;
-  prefill_attn_kernel<<<dim3(n_work, g.n_kv_heads), kThreadsAttn, smem, s>>>(
-      g, qkv, kplane, vplane, seqs, work, pages, out);
-  return cudaGetLastError();
+  return launch_pdl(prefill_attn_kernel, dim3(n_work, g.n_kv_heads), dim3(kThreadsAttn), smem, s, g, qkv,
+                    kplane, vplane, seqs, work, pages, out);
 }
 
 cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
@@ -612,15 +617,13 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (static_cast<size_t>(n_seq) * g.n_kv_heads * max_pieces * g.group * kHD > part_cap)
     return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  decode_attn_kernel<<<grid, kWarpsD * 32, smem, s>>>(g, qkv, kplane, vplane, seqs, seq_prefix, n_seq,
-                                                      total_tiles, W, pages, max_pieces, out, part_o,
-                                                      part_ml);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(decode_attn_kernel, dim3(grid), dim3(kWarpsD * 32), smem, s, g, qkv, kplane,
+                             vplane, seqs, seq_prefix, n_seq, total_tiles, W, pages, max_pieces, out,
+                             part_o, part_ml);
   if (e != cudaSuccess) return e;
   ++g_kernel_launches;
-  decode_combine_kernel<<<dim3(n_seq * g.n_kv_heads, g.group), kHD, 0, s>>>(g, seqs, seq_prefix, total_tiles, W, max_pieces,
-                                                            part_o, part_ml, out);
-  return cudaGetLastError();
+  return launch_pdl(decode_combine_kernel, dim3(n_seq * g.n_kv_heads, g.group), dim3(kHD), 0, s, g, seqs,
+                    seq_prefix, total_tiles, W, max_pieces, part_o, part_ml, out);
 }
 
 void prepare_attention_kernels() {

@@ -13,6 +13,33 @@ namespace nxd {
 // Count of kernels launched by this library (host-side, all streams).
 extern unsigned long long g_kernel_launches;
 
+// Programmatic dependent launch: every kernel of a forward is launched with
+// programmatic stream serialization, calls pdl_trigger() on entry (its
+// successor may be scheduled once all of its CTAs are resident) and
+// pdl_wait() before touching anything an upstream kernel wrote. Work that
+// needs no upstream data (barrier init, TMEM alloc, weight prefetch) runs
+// in the shadow of the previous kernel. NX_PDL=0 disables it.
+extern bool g_pdl;
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Load every kernel and set its shared-memory opt-in on the current device
 // (once per device; see kernels.cu).
 void ensure_kernels_prepared();

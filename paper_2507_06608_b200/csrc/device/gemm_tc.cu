@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) NX_STAMP(0);
+  pdl_trigger();  // let the next kernel's CTAs stage their prologue early
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tx);
     for (int s = 0; s < C::kStages; ++s) {
@@ -450,31 +451,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     if (elect_one()) {
       const uint64_t w_policy = policy_evict_first();  // weights stream once
-      int stage = 0;
+      const uint32_t stage_bytes_x = (p.dbg & 1) ? 0 : C::kBBytes;
+      // weight tiles = contiguous pre-swizzled 16 KB chunks (pack_weights); an
+      // aligned pair of row blocks is one 32 KB copy
+      auto load_w = [&](const Work& w, int kb, int valid, uint8_t* sa, uint64_t* bar) {
+        if (MT == 2 && valid == 2) {
+          bulk_load(sa, wpack + packed_tile_offset(w.m_blk * 2, kb, p.num_kb), 2 * kABytes, bar, w_policy);
+        } else {
+          for (int t = 0; t < valid; ++t)
+            bulk_load(sa + t * kABytes, wpack + packed_tile_offset(w.m_blk * MT + t, kb, p.num_kb), kABytes,
+                      bar, w_policy);
+        }
+      };
+      // 1) The weights of the first kStages fills depend on nothing upstream:
+      //    stream them before the grid dependency resolves (programmatic
+      //    dependent launch), hiding the pipeline fill behind the previous kernel.
+      int pre = 0;
+      {
+        WorkIter wp(p);
+        Work w;
+        while (pre < C::kStages && wp.next(w)) {
+          const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
+          for (int kb = w.kb0; kb < w.kb1 && pre < C::kStages; ++kb, ++pre) {
+            mbar_expect_tx(&full[pre], valid * kABytes + stage_bytes_x);
+            load_w(w, kb, valid, smem + pre * C::kStage, &full[pre]);
+          }
+        }
+      }
+      pdl_wait();  // activations below are written by the previous kernel
+      int stage = 0, fill = 0;
       uint32_t phase = 0;
       WorkIter wi(p);
       Work w;
       while (wi.next(w)) {
         const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++fill) {
           uint8_t* sa = smem + stage * C::kStage;
-          mbar_expect_tx(&full[stage], valid * kABytes + ((p.dbg & 1) ? 0 : C::kBBytes));
-          // weight tiles = contiguous pre-swizzled 16 KB chunks (pack_weights); an
-          // aligned pair of row blocks is one 32 KB copy
-          if (MT == 2 && valid == 2) {
-            bulk_load(sa, wpack + packed_tile_offset(w.m_blk * 2, kb, p.num_kb), 2 * kABytes,
-                      &full[stage], w_policy);
-          } else {
-            for (int t = 0; t < valid; ++t) {
-              const size_t off = (p.dbg & 4)
-                  ? (static_cast<size_t>(w.m_blk * MT + t) * p.num_kb + kb) * (kBM * kBK)
-                  : packed_tile_offset(w.m_blk * MT + t, kb, p.num_kb);
-              if (p.dbg & 8)
-                bulk_load(sa + t * kABytes, wpack + off, kABytes, &full[stage]);
-              else
-                bulk_load(sa + t * kABytes, wpack + off, kABytes, &full[stage], w_policy);
-            }
+          if (fill >= pre) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], valid * kABytes + stage_bytes_x);
+            load_w(w, kb, valid, sa, &full[stage]);
           }
           if (!(p.dbg & 1)) tma_load_2d(&tx, &full[stage], sa + MT * kABytes, kb * kBK, w.n_blk * BN);
           if (++stage == C::kStages) {
@@ -527,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
+    pdl_wait();  // residual / stream-K workspace come from upstream kernels
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = threadIdx.x - 64;
     const int lane = lane_id();
@@ -667,6 +684,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Folds K-split partials [split][token][rows] with the requested epilogue.
 __global__ void splitk_reduce_kernel(GemmParams p, int final_mode) {
+  pdl_trigger();
+  pdl_wait();
   const int out_cols = final_mode == kEpiSwiGLU ? p.rows / 2 : p.rows;
   const int groups = out_cols / 8;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -724,8 +743,7 @@ cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const Gemm
   using C = Cfg<BN, MT>;
   ensure_kernels_prepared();
   ++g_kernel_launches;
-  gemm_tc_kernel<BN, MT><<<grid, kThreads, C::kSmem, s>>>(tw, tx, p);
-  return cudaGetLastError();
+  return launch_pdl(gemm_tc_kernel<BN, MT>, dim3(grid), dim3(kThreads), C::kSmem, s, tw, tx, p);
 }
 
 }  // namespace
@@ -843,8 +861,7 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
   const int out_cols = mode == kEpiSwiGLU ? rows / 2 : rows;
   const int work = tokens * (out_cols / 8);
   ++g_kernel_launches;
-  splitk_reduce_kernel<<<(work + 255) / 256, 256, 0, stream>>>(p, mode);
-  return cudaGetLastError();
+  return launch_pdl(splitk_reduce_kernel, dim3((work + 255) / 256), dim3(256), 0, stream, p, mode);
 }
 
 template <int BN, int MT>

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -19,6 +20,8 @@ namespace {
 
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
                              int hidden, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<size_t>(tok[t]) * hidden);
   uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(t) * hidden);
@@ -29,6 +32,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat1
 __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows,
                                int hidden, const __nv_bfloat16* __restrict__ w, float eps,
                                __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int src_row = rows ? rows[r] : r;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(src_row) * hidden);
@@ -74,6 +79,8 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_
 // per forward and shared by all layers: table[t][j] = (cos, sin).
 __global__ void rope_table_kernel(const int32_t* __restrict__ pos, const float* __restrict__ inv_freq,
                                   int half, float2* __restrict__ table) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const float p = static_cast<float>(pos[t]);
   for (int j = threadIdx.x; j < half; j += blockDim.x) {
@@ -91,6 +98,8 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* _
                                const float2* __restrict__ table, int n_heads, int n_kv_heads,
                                int page_tokens, __nv_bfloat16* __restrict__ kplane,
                                __nv_bfloat16* __restrict__ vplane) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int hd = 128, half = 64;
   const int t = blockIdx.x;
   const int stride = (n_heads + 2 * n_kv_heads) * hd;
@@ -151,6 +160,8 @@ __device__ __forceinline__ void arg_better(float& best, int& idx, float v, int i
 
 __global__ void argmax_partial_kernel(const float* __restrict__ logits, int ld, int valid,
                                       float2* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.y, chunk = blockIdx.x;
   const int per = (valid + kArgChunks - 1) / kArgChunks;
   const int lo = chunk * per, hi = min(valid, lo + per);
@@ -176,6 +187,8 @@ __global__ void argmax_partial_kernel(const float* __restrict__ logits, int ld, 
 
 __global__ void argmax_final_kernel(const float2* __restrict__ part, int rows, int offset,
                                     int32_t* __restrict__ out, float2* __restrict__ pair_out) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -198,6 +211,8 @@ __global__ void argmax_final_kernel(const float2* __restrict__ part, int rows, i
 // TP: fold the all-gathered [tp][rows] (max, global idx) pairs.
 __global__ void argmax_fold_kernel(const float2* __restrict__ pairs, int tp, int rows,
                                    int32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= rows) return;
   float best = -FLT_MAX;
@@ -260,23 +275,23 @@ cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int 
                   __nv_bfloat16* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ++g_kernel_launches;
-  embed_kernel<<<n, 128, 0, s>>>(tokens, table, hidden, out);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3(n), dim3(128), 0, s, tokens, table, hidden, out);
 }
 
 cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows, int n, int hidden,
                     const __nv_bfloat16* w, float eps, __nv_bfloat16* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ++g_kernel_launches;
-  rmsnorm_kernel<<<n, 256, 0, s>>>(x, rows, hidden, w, eps, out);
-  return cudaGetLastError();
+  return launch_pdl(rmsnorm_kernel, dim3(n), dim3(256), 0, s, x, rows, hidden, w, eps, out);
 }
 
 cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, int head_dim,
                        float2* table, cudaStream_t s) {
   if (n_tokens == 0) return cudaSuccess;
   ++g_kernel_launches;
-  rope_table_kernel<<<n_tokens, 64, 0, s>>>(pos, inv_freq, head_dim / 2, table);
+  const cudaError_t e0 = launch_pdl(rope_table_kernel, dim3(n_tokens), dim3(64), 0, s, pos, inv_freq,
+                                    head_dim / 2, table);
+  if (e0 != cudaSuccess) return e0;
   return cudaGetLastError();
 }
 
@@ -287,25 +302,24 @@ cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* slot,
   if (n_tokens == 0) return cudaSuccess;
   if (head_dim != 128) return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  rope_kv_kernel<<<n_tokens, 128, 0, s>>>(qkv, slot, table, n_heads, n_kv_heads, page_tokens,
-                                          kplane, vplane);
-  return cudaGetLastError();
+  return launch_pdl(rope_kv_kernel, dim3(n_tokens), dim3(128), 0, s, qkv, slot, table, n_heads, n_kv_heads,
+                    page_tokens, kplane, vplane);
 }
 
 cudaError_t argmax_rows(const float* logits, int n, int ld, int valid, int offset, int32_t* out,
                         float2* pair_out, float2* scratch, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   g_kernel_launches += 2;
-  argmax_partial_kernel<<<dim3(kArgChunks, n), 256, 0, s>>>(logits, ld, valid, scratch);
-  argmax_final_kernel<<<(n + 7) / 8, 256, 0, s>>>(scratch, n, offset, out, pair_out);
-  return cudaGetLastError();
+  const cudaError_t e = launch_pdl(argmax_partial_kernel, dim3(kArgChunks, n), dim3(256), 0, s, logits, ld,
+                                   valid, scratch);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(argmax_final_kernel, dim3((n + 7) / 8), dim3(256), 0, s, scratch, n, offset, out, pair_out);
 }
 
 cudaError_t argmax_fold(const float2* pairs, int tp, int rows, int32_t* out, cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
   ++g_kernel_launches;
-  argmax_fold_kernel<<<(rows + 127) / 128, 128, 0, s>>>(pairs, tp, rows, out);
-  return cudaGetLastError();
+  return launch_pdl(argmax_fold_kernel, dim3((rows + 127) / 128), dim3(128), 0, s, pairs, tp, rows, out);
 }
 
 cudaError_t fill_random(__nv_bfloat16* p, size_t n, uint64_t seed, float scale, float offset,
@@ -341,6 +355,11 @@ bool encode_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
 // idle. A TP rank spinning in a peer collective never lets it go idle, so
 // every kernel (and its smem opt-in, which is per device) is prepared up
 // front on each device the library runs on.
+bool g_pdl = [] {
+  const char* e = std::getenv("NX_PDL");
+  return !(e && e[0] == '0');
+}();
+
 void ensure_kernels_prepared() {
   static std::atomic<uint64_t> mask{0};
   int d = 0;

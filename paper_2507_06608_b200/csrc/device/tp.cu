@@ -165,6 +165,7 @@ __device__ __forceinline__ void peer_barrier(const PeerArgs& a, int chunk) {
 }
 
 __global__ void peer_allreduce_kernel(PeerArgs a, __nv_bfloat16* x) {
+  pdl_wait();
   const size_t v0 = (blockIdx.x * a.chunk) / 8, v1 = min(a.n, (blockIdx.x + 1) * a.chunk) / 8;
   uint4* mine = static_cast<uint4*>(a.mine);
   const uint4* xv = reinterpret_cast<const uint4*>(x);
@@ -192,6 +193,7 @@ __global__ void peer_allreduce_kernel(PeerArgs a, __nv_bfloat16* x) {
 }
 
 __global__ void peer_argmax_kernel(PeerArgs a, const float2* mine_pairs, int32_t* out) {
+  pdl_wait();
   float2* mine = static_cast<float2*>(a.mine);
   for (int i = threadIdx.x; i < static_cast<int>(a.n); i += blockDim.x) mine[i] = mine_pairs[i];
   peer_barrier(a, 0);
