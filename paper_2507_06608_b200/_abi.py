@@ -11,7 +11,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libnexus_b200.so")
+LIB_PATH = os.environ.get("NX_LIB_PATH") or os.path.join(HERE, "libnexus_b200.so")  # override: A/B experiments
 
 NX_OK, NX_EINVAL, NX_ERUNTIME, NX_ENOMEM, NX_EAGAIN, NX_EDONE, NX_ENODEV = range(7)
 NX_ENGINE_NEXUS, NX_ENGINE_MONOLITHIC, NX_ENGINE_STATIC = 0, 1, 2

@@ -564,6 +564,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int f0 = m128 * kBM;
         const int tok0 = w.n_blk * BN + c0;
         if (tok0 >= p.tokens) break;
+        // residual rows of this 32-token chunk: issued before the TMEM load
+        // so their global latency overlaps the accumulator staging
+        const bool has_res = !w.partial && (p.mode == kEpiResidual || p.mode == kEpiBiasResidual);
+        uint4 res[4];
+        if (has_res) {
+          const int g = et & 15;
+#pragma unroll
+          for (int pass = 0; pass < 4; ++pass) {
+            const int t = tok0 + pass * 8 + (et >> 4);
+            res[pass] = t < p.tokens ? *reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(t) * p.ldr +
+                                                                      f0 + g * 8)
+                                     : make_uint4(0, 0, 0, 0);
+          }
+        }
         uint32_t r[32];
         tmem_ld32(tmem + (acc * MT + sub) * BN + c0 + (static_cast<uint32_t>(q * 32) << 16), r);
         tmem_ld_wait();
@@ -634,10 +648,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] += bf2f(bb[i]);
               }
-              if (p.mode == kEpiResidual || p.mode == kEpiBiasResidual) {
-                const uint4 rr = *reinterpret_cast<const uint4*>(
-                    p.residual + static_cast<size_t>(t) * p.ldr + f);
-                const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rr);
+              if (has_res) {
+                const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&res[pass]);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] += bf2f(rb[i]);
               }
