@@ -311,8 +311,17 @@ def main():
         m["launches"] = eng.stats().launches
         m["h2d"] = sum(4 * t.prompt_len for t in trace)
         m["d2h"] = 4 * sum(len(x) - t.prompt_len for x, t in zip(toks, trace))
-        m["decisions"] = eng.decision_log().count("\n") - 1
+        dlog = eng.decision_log()
+        m["decisions"] = dlog.count("\n") - 1
         m["switches"] = eng.stats().switches
+        # applied prefill share of the decisions taken while requests arrive
+        t_end = trace[-1].arrival_s
+        hist = {}
+        for line in dlog.splitlines()[1:]:
+            f = line.split("\t")
+            if float(f[0]) <= t_end:
+                hist[int(f[4])] = hist.get(int(f[4]), 0) + 1
+        m["r_p_hist"] = hist
         eng.close()
         return m
 
@@ -414,6 +423,8 @@ def main():
         "output_tokens": out_tok, "slo_attainment": good / out_tok if out_tok else 0.0,
         "throughput_makespan": out_tok / (span_sum / world) if span_sum else 0.0,
         "decisions": sum(r["decisions"] for r in results), "switches": sum(r["switches"] for r in results),
+        "r_p_hist_arrivals": {str(k): sum(r["r_p_hist"].get(k, 0) for r in results)
+                              for k in sorted({k for r in results for k in r["r_p_hist"]})},
         "e2e": {"value": e2e, "unit": "tok/s", "h2d_bytes_per_step": sum(r["h2d"] for r in results) // args.steps,
                 "d2h_bytes_per_step": sum(r["d2h"] for r in results) // args.steps},
         "gpu_launches": int(ks.kernel_launches - k0),

@@ -75,6 +75,7 @@ struct GemmParams {
   int n_tiles128;  // 128-row weight blocks (n_mblk counts MT-block work tiles)
   int coresident;  // stream-K: parallel reduce-scatter fix-up (see gemm())
   int dbg;         // experiments only (NX_GEMM_DBG): 1 skip X loads, 2 skip MMAs
+  int fold;        // 1: every work item writes fp32 planes, no fix-up (see GemmFold)
 };
 
 int gemm_pick_bn(int tokens);
@@ -92,10 +93,38 @@ cudaError_t unpack_weights(const __nv_bfloat16* src, __nv_bfloat16* dst, int row
                            cudaStream_t s);
 // ws must start with gemm_counter_bytes() of zeroed int counters (kept zero
 // by the kernel itself between launches on the same stream).
+// Deferred-fold output of a decode-shaped GEMM: instead of a cross-CTA
+// fix-up inside the GEMM (a chain of dependent global round trips, ~5 us of
+// its critical path), every work item writes its fp32 accumulator to plane
+// `piece` ([piece][tokens][rows]) and the consumer kernel (fold_*) sums the
+// planes of each element in piece order, applying the epilogue there.
+struct GemmFold {
+  const float* planes = nullptr;
+  int rows = 0, tokens = 0;
+  int kind = 0;      // 0: one plane; 1: `splits` uniform K splits; 2: stream-K pieces
+  int splits = 1;
+  int n_nblk = 1, num_kb = 1, grid = 1, rows_per_blk = 128, bn = 32;
+  long long total = 1;  // stream-K (tile, k-block) iterations
+};
+#ifdef __CUDACC__
+// Number of planes holding a partial of element (row, token t).
+__device__ __forceinline__ int fold_pieces(const GemmFold& f, int row, int t) {
+  if (f.kind == 0) return 1;
+  if (f.kind == 1) return f.splits;
+  const int tile = (row / f.rows_per_blk) * f.n_nblk + t / f.bn;
+  const long long it0 = static_cast<long long>(tile) * f.num_kb;
+  const int first = static_cast<int>(((it0 + 1) * f.grid - 1) / f.total);
+  const int last = static_cast<int>(((it0 + f.num_kb) * f.grid - 1) / f.total);
+  return last - first + 1;
+}
+#endif
+// fold != nullptr: deferred-fold mode (mode/out/bias/residual are ignored;
+// the consumer applies them); *fold describes the planes written.
 cudaError_t gemm(const __nv_bfloat16* w_packed, const CUtensorMap& x_map, int bn, int rows, int tokens,
                  int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
                  const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
-                 cudaStream_t stream, int force_splits = 0, bool coresident = false);
+                 cudaStream_t stream, int force_splits = 0, bool coresident = false,
+                 GemmFold* fold = nullptr);
 // coresident: the launch owns its SMs (green-context partition, or nothing
 // else running), so every CTA of the persistent grid is resident at once and
 // stream-K pieces may wait for each other (parallel fix-up); otherwise the
@@ -151,6 +180,16 @@ cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, 
                        float2* table, cudaStream_t s);
 // Rotary embedding on q and k (rotate-half pairs), then k, v -> paged cache
 // in the pre-swizzled page layout the attention kernels bulk-copy.
+// Consumers of deferred-fold GEMM planes (one launch each, PDL):
+//  x = bf16(x + sum planes); h = rmsnorm(x) * w (skipped when w == nullptr)
+cudaError_t fold_residual_rmsnorm(const GemmFold& f, __nv_bfloat16* x, const __nv_bfloat16* w, float eps,
+                                  __nv_bfloat16* h, cudaStream_t s);
+//  act[t][64 b + i] = silu(sum gate row 128 b + i) * (sum up row 128 b + 64 + i)
+cudaError_t fold_swiglu(const GemmFold& f, __nv_bfloat16* act, cudaStream_t s);
+//  qkv row = bf16(sum planes + bias), then RoPE + paged KV write as rope_kv_write
+cudaError_t fold_rope_kv(const GemmFold& f, const __nv_bfloat16* bias, __nv_bfloat16* qkv,
+                         const int32_t* slot, const float2* table, int n_heads, int n_kv_heads,
+                         int page_tokens, __nv_bfloat16* kplane, __nv_bfloat16* vplane, cudaStream_t s);
 cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* slot,
                           const float2* table, int n_heads, int n_kv_heads, int head_dim,
                           int page_tokens, __nv_bfloat16* kplane, __nv_bfloat16* vplane,

@@ -125,6 +125,7 @@ __device__ __forceinline__ Unit unit_of(int u, const GemmParams& p) {
 struct Work {
   int m_blk, n_blk, kb0, kb1;
   int slot;      // stream-K: partial slot (tile * max_pieces + piece); split-K: split index
+  int piece;     // fold planes: stream-K piece within the tile / split index / 0
   bool partial;  // true: write fp32 partials for a fix-up pass
 };
 
@@ -155,10 +156,12 @@ struct WorkIter {
       w.m_blk = tile / p.n_nblk;
       w.partial = !(w.kb0 == 0 && w.kb1 == p.num_kb);
       w.slot = -1;
+      w.piece = 0;
       if (w.partial) {
         const long long it0 = static_cast<long long>(tile) * p.num_kb;
         const int first = static_cast<int>(((it0 + 1) * gridDim.x - 1) / total);
-        w.slot = tile * p.max_pieces + (static_cast<int>(blockIdx.x) - first);
+        w.piece = static_cast<int>(blockIdx.x) - first;
+        w.slot = tile * p.max_pieces + w.piece;
       }
       it += w.kb1 - w.kb0;
       return true;
@@ -171,6 +174,7 @@ struct WorkIter {
     w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
     w.partial = p.splits > 1;
     w.slot = x.split;
+    w.piece = x.split;
     u += gridDim.x;
     return true;
   }
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tok0 >= p.tokens) break;
         // residual rows of this 32-token chunk: issued before the TMEM load
         // so their global latency overlaps the accumulator staging
-        const bool has_res = !w.partial && (p.mode == kEpiResidual || p.mode == kEpiBiasResidual);
+        const bool has_res = !w.partial && !p.fold && (p.mode == kEpiResidual || p.mode == kEpiBiasResidual);
         uint4 res[4];
         if (has_res) {
           const int g = et & 15;
@@ -584,8 +588,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) s_epi[j * kBM + q * 32 + lane] = __uint_as_float(r[j]);
         named_bar_sync(1, kEpiThreads);
-        if (w.partial) {
-          // fp32 partials: stream-K slot [BN tokens][128] or split-K plane
+        if (w.partial || p.fold) {
+          // fp32 partials: fold plane [piece][token][rows], stream-K slot
+          // [BN tokens][128] or split-K plane
           const int g = et & 31;
 #pragma unroll
           for (int pass = 0; pass < 8; ++pass) {
@@ -593,9 +598,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int t = tok0 + j;
             if (t < p.tokens) {
               const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
-              float* dst = p.streamk
-                               ? p.ws + ((static_cast<size_t>(w.slot) * MT + sub) * BN + c0 + j) * kBM + g * 4
-                               : p.ws + (static_cast<size_t>(w.slot) * p.tokens + t) * p.rows + f0 + g * 4;
+              float* dst =
+                  p.fold      ? p.ws + (static_cast<size_t>(w.piece) * p.tokens + t) * p.rows + f0 + g * 4
+                  : p.streamk ? p.ws + ((static_cast<size_t>(w.slot) * MT + sub) * BN + c0 + j) * kBM + g * 4
+                              : p.ws + (static_cast<size_t>(w.slot) * p.tokens + t) * p.rows + f0 + g * 4;
               *reinterpret_cast<float4*>(dst) = v;
             }
           }
@@ -667,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (et == 0) NX_STAMP(5);
-      if (p.streamk && w.partial) {
+      if (p.streamk && w.partial && !p.fold) {
         if (p.coresident && n_pend < 2) {
           // publish now, fold after the last item: publishing never waits,
           // so no chain of waits can form across CTAs
@@ -789,7 +795,7 @@ int gemm_pick_bn(int tokens) {
 cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, int bn, int rows,
                  int tokens, int K, int mode, void* out, int ldo, const __nv_bfloat16* bias,
                  const __nv_bfloat16* residual, int ldr, float* ws, size_t ws_bytes, int sm_count,
-                 cudaStream_t stream, int force_splits, bool coresident) {
+                 cudaStream_t stream, int force_splits, bool coresident, GemmFold* fold) {
   if (tokens <= 0) return cudaSuccess;
   if (rows % kBM || K % kBK) return cudaErrorInvalidValue;
   GemmParams p{};
@@ -818,6 +824,7 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
   }();
   p.dbg = dbg;
   p.coresident = coresident ? 1 : 0;
+  p.fold = fold ? 1 : 0;
   // ws layout: [int tile counters | fp32 partials]
   p.tile_count = reinterpret_cast<int*>(ws);
   p.ws = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + gemm_counter_bytes()) : nullptr;
@@ -828,7 +835,48 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
   p.splits = 1;
   p.kb_per_split = p.num_kb;
   p.streamk = 0;
-  if (force_splits > 0) {
+  const size_t plane_bytes = static_cast<size_t>(tokens) * rows * 4;
+  if (fold) {
+    // Deferred fold: planes only, no counters, no fix-up, no reduce kernel.
+    GemmFold f;
+    f.planes = p.ws;
+    f.rows = rows;
+    f.tokens = tokens;
+    f.rows_per_blk = kBM * mt;
+    f.bn = bn;
+    f.n_nblk = p.n_nblk;
+    f.num_kb = p.num_kb;
+    if (p.ws == nullptr || plane_bytes > ws_bytes) return cudaErrorInvalidValue;
+    const int max_splits = static_cast<int>(std::min<size_t>(64, ws_bytes / plane_bytes));
+    int splits = force_splits > 0 ? force_splits
+                 : (mt == 2 && tiles < sm_count) ? std::min((sm_count + tiles - 1) / tiles, std::max(1, p.num_kb / 8))
+                                                 : 0;
+    if (splits > 0) {
+      splits = std::min(splits, max_splits);
+      p.kb_per_split = (p.num_kb + splits - 1) / splits;
+      p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+      grid = std::max(1, std::min(tiles * p.splits, sm_count));
+      f.kind = p.splits > 1 ? 1 : 0;
+      f.splits = p.splits;
+    } else {
+      grid = std::max(1, std::min(tiles, sm_count));
+      if (tiles % sm_count != 0 && tiles < 8 * sm_count) {
+        // stream-K: equal (tile, k-block) ranges per CTA (no wave tail)
+        const int G = static_cast<int>(std::min<long long>(sm_count, iters));
+        const long long per_min = iters / G;
+        const int max_pieces = static_cast<int>((p.num_kb + per_min - 1) / per_min) + 1;
+        if (max_pieces <= max_splits) {
+          p.streamk = 1;
+          p.max_pieces = max_pieces;
+          grid = G;
+          f.kind = 2;
+          f.grid = G;
+          f.total = iters;
+        }
+      }
+    }
+    *fold = f;
+  } else if (force_splits > 0) {
     // explicit split-K (tests / experiments)
     p.kb_per_split = (p.num_kb + force_splits - 1) / force_splits;
     p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
@@ -869,7 +917,7 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
-  if (p.streamk || p.splits == 1) return cudaSuccess;
+  if (fold || p.streamk || p.splits == 1) return cudaSuccess;
   const int out_cols = mode == kEpiSwiGLU ? rows / 2 : rows;
   const int work = tokens * (out_cols / 8);
   ++g_kernel_launches;

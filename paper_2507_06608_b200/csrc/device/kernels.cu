@@ -90,30 +90,24 @@ __global__ void rope_table_kernel(const int32_t* __restrict__ pos, const float* 
   }
 }
 
-// One CTA per token. Work items: (q or k head, chunk pair p) rotates dims
-// [8p, 8p+8) with [64+8p, 64+8p+8) (rotate-half, hd = 128) using 16 B
-// vectors; q stays in the qkv buffer, k and v go to the paged cache in the
-// pre-swizzled layout (16 B chunk c of page row r at c ^ (r & 7)).
-__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ slot,
-                               const float2* __restrict__ table, int n_heads, int n_kv_heads,
-                               int page_tokens, __nv_bfloat16* __restrict__ kplane,
-                               __nv_bfloat16* __restrict__ vplane) {
-  pdl_trigger();
-  pdl_wait();
+// One token's RoPE + paged KV write. Work items: (q or k head, chunk pair p)
+// rotates dims [8p, 8p+8) with [64+8p, 64+8p+8) (rotate-half, hd = 128)
+// using 16 B vectors; q goes to qdst (the qkv row the attention reads), k and
+// v go to the paged cache in the pre-swizzled layout (16 B chunk c of page
+// row r at c ^ (r & 7)). `row` may live in global or shared memory.
+__device__ __forceinline__ void rope_kv_token(const __nv_bfloat16* row, __nv_bfloat16* qdst, int s,
+                                              const float2* __restrict__ cs, int n_heads, int n_kv_heads,
+                                              int page_tokens, __nv_bfloat16* __restrict__ kplane,
+                                              __nv_bfloat16* __restrict__ vplane) {
   constexpr int hd = 128, half = 64;
-  const int t = blockIdx.x;
-  const int stride = (n_heads + 2 * n_kv_heads) * hd;
-  __nv_bfloat16* row = qkv + static_cast<size_t>(t) * stride;
-  const int s = slot[t];
   const int page = s / page_tokens, off = s % page_tokens;
   const int sw = off & 7;
-  const float2* cs = table + static_cast<size_t>(t) * half;
   const int rot_items = (n_heads + n_kv_heads) * 8;
   const int v_items = n_kv_heads * 16;
   for (int it = threadIdx.x; it < rot_items + v_items; it += blockDim.x) {
     if (it < rot_items) {
       const int head = it >> 3, p = it & 7;
-      __nv_bfloat16* h = row + head * hd;
+      const __nv_bfloat16* h = row + head * hd;
       const uint4 va = *reinterpret_cast<const uint4*>(h + 8 * p);
       const uint4 vb = *reinterpret_cast<const uint4*>(h + half + 8 * p);
       const __nv_bfloat16* a = reinterpret_cast<const __nv_bfloat16*>(&va);
@@ -127,8 +121,8 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* _
         rb[i] = __float2bfloat16(y * c.x + x * c.y);
       }
       if (head < n_heads) {
-        *reinterpret_cast<uint4*>(h + 8 * p) = *reinterpret_cast<uint4*>(ra);
-        *reinterpret_cast<uint4*>(h + half + 8 * p) = *reinterpret_cast<uint4*>(rb);
+        *reinterpret_cast<uint4*>(qdst + head * hd + 8 * p) = *reinterpret_cast<uint4*>(ra);
+        *reinterpret_cast<uint4*>(qdst + head * hd + half + 8 * p) = *reinterpret_cast<uint4*>(rb);
       } else {
         __nv_bfloat16* dst =
             kplane + ((static_cast<size_t>(page) * n_kv_heads + (head - n_heads)) * page_tokens + off) * hd;
@@ -144,6 +138,141 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* _
       *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 3)) = *reinterpret_cast<const uint4*>(src);
     }
   }
+}
+
+// One CTA per token: RoPE on q (in place) and k, k/v -> paged cache.
+__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ slot,
+                               const float2* __restrict__ table, int n_heads, int n_kv_heads,
+                               int page_tokens, __nv_bfloat16* __restrict__ kplane,
+                               __nv_bfloat16* __restrict__ vplane) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x;
+  __nv_bfloat16* row = qkv + static_cast<size_t>(t) * (n_heads + 2 * n_kv_heads) * 128;
+  rope_kv_token(row, row, slot[t], table + static_cast<size_t>(t) * 64, n_heads, n_kv_heads, page_tokens,
+                kplane, vplane);
+}
+
+// ---- consumers of deferred-fold GEMM planes ---------------------------------
+// Sum of the fp32 partials of elements [row, row + 8) of token t, in piece
+// order (deterministic for a given partition).
+__device__ __forceinline__ void fold8(const GemmFold& f, int row, int t, float (&v)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 0.f;
+  const int n = fold_pieces(f, row, t);
+  const size_t plane = static_cast<size_t>(f.tokens) * f.rows;
+  const float* src = f.planes + static_cast<size_t>(t) * f.rows + row;
+  for (int q = 0; q < n; ++q) {
+    const float4 a = __ldcg(reinterpret_cast<const float4*>(src + q * plane));
+    const float4 b = __ldcg(reinterpret_cast<const float4*>(src + q * plane + 4));
+    v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
+    v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+  }
+}
+
+// One CTA (256 threads) per token; hidden <= 256 * 8 * kFoldVec.
+constexpr int kFoldVec = 4;
+__global__ void __launch_bounds__(256) fold_residual_rmsnorm_kernel(GemmFold f, __nv_bfloat16* __restrict__ x,
+                                                                    const __nv_bfloat16* __restrict__ w, float eps,
+                                                                    __nv_bfloat16* __restrict__ h) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x, d = f.rows;
+  __nv_bfloat16* xr = x + static_cast<size_t>(t) * d;
+  float keep[kFoldVec][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int c = 0; c < kFoldVec; ++c) {
+    const int row = (threadIdx.x + c * 256) * 8;
+    if (row >= d) break;
+    float v[8];
+    fold8(f, row, t, v);
+    const uint4 rv = *reinterpret_cast<const uint4*>(xr + row);
+    const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i] = __float2bfloat16(v[i] + __bfloat162float(rb[i]));  // the GEMM residual epilogue
+      keep[c][i] = __bfloat162float(o[i]);
+      ss += keep[c][i] * keep[c][i];
+    }
+    *reinterpret_cast<uint4*>(xr + row) = *reinterpret_cast<uint4*>(o);
+  }
+  if (w == nullptr) return;
+  __shared__ float red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) tot += red[i];
+  const float inv = rsqrtf(tot / d + eps);
+  __nv_bfloat16* hr = h + static_cast<size_t>(t) * d;
+#pragma unroll
+  for (int c = 0; c < kFoldVec; ++c) {
+    const int row = (threadIdx.x + c * 256) * 8;
+    if (row >= d) break;
+    const uint4 wv = *reinterpret_cast<const uint4*>(w + row);
+    const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(&wv);
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(keep[c][i] * inv * __bfloat162float(wb[i]));
+    *reinterpret_cast<uint4*>(hr + row) = *reinterpret_cast<uint4*>(o);
+  }
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+// grid (ceil(ffn / 2048), tokens): thread = 8 consecutive outputs.
+__global__ void __launch_bounds__(256) fold_swiglu_kernel(GemmFold f, __nv_bfloat16* __restrict__ act) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.y;
+  const int ffn = f.rows / 2;
+  const int j = (blockIdx.x * 256 + threadIdx.x) * 8;
+  if (j >= ffn) return;
+  const int rg = (j >> 6) * 128 + (j & 63);  // gate rows of 128-row block j / 64; up = +64
+  float g[8], u[8];
+  fold8(f, rg, t, g);
+  fold8(f, rg + 64, t, u);
+  __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(silu_f(g[i]) * u[i]);
+  *reinterpret_cast<uint4*>(act + static_cast<size_t>(t) * ffn + j) = *reinterpret_cast<uint4*>(o);
+}
+
+// One CTA per token: the qkv row is folded into shared memory (+ bias,
+// rounded to bf16 exactly like the GEMM's bias/store epilogue), then RoPE
+// and the paged KV write run on it.
+__global__ void __launch_bounds__(256) fold_rope_kv_kernel(GemmFold f, const __nv_bfloat16* __restrict__ bias,
+                                                           __nv_bfloat16* __restrict__ qkv,
+                                                           const int32_t* __restrict__ slot,
+                                                           const float2* __restrict__ table, int n_heads,
+                                                           int n_kv_heads, int page_tokens,
+                                                           __nv_bfloat16* __restrict__ kplane,
+                                                           __nv_bfloat16* __restrict__ vplane) {
+  extern __shared__ __align__(16) __nv_bfloat16 srow[];
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x;
+  for (int row = threadIdx.x * 8; row < f.rows; row += blockDim.x * 8) {
+    float v[8];
+    fold8(f, row, t, v);
+    if (bias) {
+      const uint4 bv = *reinterpret_cast<const uint4*>(bias + row);
+      const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&bv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += __bfloat162float(bb[i]);
+    }
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(v[i]);
+    *reinterpret_cast<uint4*>(srow + row) = *reinterpret_cast<uint4*>(o);
+  }
+  __syncthreads();
+  rope_kv_token(srow, qkv + static_cast<size_t>(t) * f.rows, slot[t], table + static_cast<size_t>(t) * 64,
+                n_heads, n_kv_heads, page_tokens, kplane, vplane);
 }
 
 // Greedy sampling, two passes: kArgChunks CTAs per row reduce a slice of
@@ -295,6 +424,32 @@ cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, 
   return cudaGetLastError();
 }
 
+cudaError_t fold_residual_rmsnorm(const GemmFold& f, __nv_bfloat16* x, const __nv_bfloat16* w, float eps,
+                                  __nv_bfloat16* h, cudaStream_t s) {
+  if (f.tokens == 0) return cudaSuccess;
+  if (f.rows % 8 || f.rows > 256 * 8 * kFoldVec) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  return launch_pdl(fold_residual_rmsnorm_kernel, dim3(f.tokens), dim3(256), 0, s, f, x, w, eps, h);
+}
+
+cudaError_t fold_swiglu(const GemmFold& f, __nv_bfloat16* act, cudaStream_t s) {
+  if (f.tokens == 0) return cudaSuccess;
+  const int ffn = f.rows / 2;
+  if (f.rows % 128) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  return launch_pdl(fold_swiglu_kernel, dim3((ffn + 2047) / 2048, f.tokens), dim3(256), 0, s, f, act);
+}
+
+cudaError_t fold_rope_kv(const GemmFold& f, const __nv_bfloat16* bias, __nv_bfloat16* qkv,
+                         const int32_t* slot, const float2* table, int n_heads, int n_kv_heads,
+                         int page_tokens, __nv_bfloat16* kplane, __nv_bfloat16* vplane, cudaStream_t s) {
+  if (f.tokens == 0) return cudaSuccess;
+  if (f.rows != (n_heads + 2 * n_kv_heads) * 128) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  return launch_pdl(fold_rope_kv_kernel, dim3(f.tokens), dim3(256), static_cast<size_t>(f.rows) * 2, s, f, bias,
+                    qkv, slot, table, n_heads, n_kv_heads, page_tokens, kplane, vplane);
+}
+
 cudaError_t rope_kv_write(__nv_bfloat16* qkv, int n_tokens, const int32_t* slot,
                           const float2* table, int n_heads, int n_kv_heads, int head_dim,
                           int page_tokens, __nv_bfloat16* kplane, __nv_bfloat16* vplane,
@@ -378,6 +533,9 @@ void ensure_kernels_prepared() {
                        reinterpret_cast<const void*>(rmsnorm_kernel),
                        reinterpret_cast<const void*>(rope_table_kernel),
                        reinterpret_cast<const void*>(rope_kv_kernel),
+                       reinterpret_cast<const void*>(fold_residual_rmsnorm_kernel),
+                       reinterpret_cast<const void*>(fold_swiglu_kernel),
+                       reinterpret_cast<const void*>(fold_rope_kv_kernel),
                        reinterpret_cast<const void*>(argmax_partial_kernel),
                        reinterpret_cast<const void*>(argmax_final_kernel),
                        reinterpret_cast<const void*>(argmax_fold_kernel)};

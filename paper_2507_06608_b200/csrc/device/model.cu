@@ -541,23 +541,40 @@ void Model::forward(LaneWs& ws) {
   timed(NX_K_OTHER, Td * a_.head_dim * 4, 0, [&] {
     ck(rope_table(ws.d_pos, T, inv_freq_, a_.head_dim, ws.rope_cs, s), "rope table");
   });
+  // Decode-shaped batches defer the GEMMs' cross-CTA K fold to the consumer
+  // kernel (GemmFold): residual + RMSNorm, SwiGLU and bias + RoPE + KV write
+  // each read the fp32 planes, so no GEMM waits on a fix-up round trip and
+  // the separate RMSNorm / RoPE launches disappear.
+  const bool fold = fold_enabled_ && tp_ == 1 && T <= 128;
+  GemmFold fq, fo, fg, fd;
+  // bytes of the planes a fold reads: pieces <= ~max planes; count one plane
+  auto pbytes = [&](double rows) { return Td * rows * 4; };
   for (int l = 0; l < a_.n_layers; ++l) {
     const LayerW& w = layers_[l];
     __nv_bfloat16* kplane = kv_ + (2 * static_cast<size_t>(l)) * plane_elems_;
     __nv_bfloat16* vplane = kplane + plane_elems_;
-    timed(NX_K_OTHER, Td * d * 4, 0, [&] {
-      ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
-    });
-    timed(gk, gbytes(qkv_rows_, d, 2, false), gflops(qkv_rows_, d), [&] {
+    if (!fold || l == 0)
+      timed(NX_K_OTHER, Td * d * 4, 0, [&] {
+        ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
+      });
+    timed(gk, gbytes(qkv_rows_, d, fold ? 4 : 2, false), gflops(qkv_rows_, d), [&] {
       ck(gemm(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
-              ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
+              ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive,
+              fold ? &fq : nullptr),
          "qkv gemm");
     });
-    timed(NX_K_OTHER, Td * qkv_rows_ * 4, 0, [&] {
-      ck(rope_kv_write(ws.qkv, T, ws.d_slot, ws.rope_cs, hq_, hkv_, a_.head_dim,
-                       cfg_.page_tokens, kplane, vplane, s),
-         "rope");
-    });
+    if (fold)
+      timed(NX_K_OTHER, pbytes(qkv_rows_) + Td * qkv_rows_ * 2, 0, [&] {
+        ck(fold_rope_kv(fq, w.qkv_bias, ws.qkv, ws.d_slot, ws.rope_cs, hq_, hkv_, cfg_.page_tokens, kplane,
+                        vplane, s),
+           "fold rope");
+      });
+    else
+      timed(NX_K_OTHER, Td * qkv_rows_ * 4, 0, [&] {
+        ck(rope_kv_write(ws.qkv, T, ws.d_slot, ws.rope_cs, hq_, hkv_, a_.head_dim,
+                         cfg_.page_tokens, kplane, vplane, s),
+           "rope");
+      });
     if (ws.dec_seq_count > 0)
       timed(NX_K_ATTN_DECODE, ws.dec_kv_tokens * kvtok + ws.dec_seq_count * qo,
             4.0 * ws.dec_kv_tokens * attn_cols_, [&] {
@@ -576,26 +593,42 @@ void Model::forward(LaneWs& ws) {
     // Row-parallel under TP: rank 0 adds the residual, the others store
     // their partial; the all-reduce then yields x + sum_r o_r on every rank.
     const int res_mode = (tp_ == 1 || rank_ == 0) ? kEpiResidual : kEpiStore;
-    timed(gk, gbytes(d, attn_cols_, 2, true), gflops(d, attn_cols_), [&] {
+    timed(gk, gbytes(d, attn_cols_, fold ? 4 : 2, !fold), gflops(d, attn_cols_), [&] {
       ck(gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x,
-              d, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
+              d, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive, fold ? &fo : nullptr),
          "o gemm");
     });
     if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
-    timed(NX_K_OTHER, Td * d * 4, 0, [&] {
-      ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
-    });
-    timed(gk, gbytes(2.0 * ffn_, d, 1, false), gflops(2.0 * ffn_, d), [&] {
+    if (fold)
+      timed(NX_K_OTHER, pbytes(d) + Td * d * 6, 0, [&] {
+        ck(fold_residual_rmsnorm(fo, ws.x, w.ffn_norm, a_.rms_eps, ws.h, s), "fold o");
+      });
+    else
+      timed(NX_K_OTHER, Td * d * 4, 0, [&] {
+        ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
+      });
+    timed(gk, gbytes(2.0 * ffn_, d, fold ? 8 : 1, false), gflops(2.0 * ffn_, d), [&] {
       ck(gemm(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr,
-              nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
+              nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive, fold ? &fg : nullptr),
          "gate/up gemm");
     });
-    timed(gk, gbytes(d, ffn_, 2, true), gflops(d, ffn_), [&] {
+    if (fold)
+      timed(NX_K_OTHER, pbytes(2.0 * ffn_) + Td * ffn_ * 2, 0, [&] {
+        ck(fold_swiglu(fg, ws.act, s), "fold swiglu");
+      });
+    timed(gk, gbytes(d, ffn_, fold ? 4 : 2, !fold), gflops(d, ffn_), [&] {
       ck(gemm(w.down, ws.map_act[bi], bn, d, T, ffn_, res_mode, ws.x, d, nullptr, ws.x, d,
-              ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
+              ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive, fold ? &fd : nullptr),
          "down gemm");
     });
     if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
+    if (fold) {
+      // the next layer's attention RMSNorm rides along (none after the last)
+      const __nv_bfloat16* next_norm = l + 1 < a_.n_layers ? layers_[l + 1].attn_norm : nullptr;
+      timed(NX_K_OTHER, pbytes(d) + Td * d * 6, 0, [&] {
+        ck(fold_residual_rmsnorm(fd, ws.x, next_norm, a_.rms_eps, ws.h, s), "fold down");
+      });
+    }
   }
   // lm_head over the sampled rows, in chunks of the logits buffer.
   ws.d_out_tokens = ws.logits_tokens_dev();

@@ -1,6 +1,8 @@
 // Device executor declarations (see model.cu).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -166,6 +168,11 @@ class Model : public nxb::Executor {
   uint64_t weight_bytes_ = 0, kv_bytes_ = 0;
   LaneWs lanes_[2];
   int sample_every_ = 0;
+  // deferred-fold decode GEMMs (GemmFold); NX_FOLD=0 restores the in-GEMM fix-up
+  bool fold_enabled_ = [] {
+    const char* e = std::getenv("NX_FOLD");
+    return !(e && e[0] == '0');
+  }();
   nx_kernel_stats kstats_{};
 };
 

@@ -7,7 +7,7 @@ from paper_2507_06608_b200 import device as D
 B = int(os.environ.get("B", "64")); CTX = int(os.environ.get("CTX", "600"))
 DPCT = int(os.environ.get("DPCT", "100")); PPCT = int(os.environ.get("PPCT", "100"))
 REPS = int(os.environ.get("REPS", "3")); MODE = os.environ.get("MODE", "decode")
-dev = D.Device(D.arch_preset("llama3-8b"), num_pages=B * (CTX // 16 + 2) + 600)
+dev = D.Device(D.arch_preset("llama3-8b"), num_pages=B * (CTX // 16 + 2) + 600, max_decode_batch=max(64, B))
 rng = np.random.default_rng(0)
 pp = CTX // 16 + 2
 Dm = [dict(tokens=[int(rng.integers(0, 1000))], start=CTX - 1, pages=list(range(i * pp, (i + 1) * pp))) for i in range(B)]
