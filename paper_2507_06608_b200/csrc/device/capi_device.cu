@@ -184,10 +184,53 @@ size_t nx_dbg_gemm_trace(uint64_t* out, size_t n) {
   return nxd::gemm_trace_read(reinterpret_cast<unsigned long long*>(out), n);
 }
 
+// Decode GEMM (tokens <= 128): mode 16 = stream-K fold planes + fold_store_f32,
+// mode 17 = direct fp32 (data-parallel). out is fp32 [tokens][rows].
+static int op_gemm_decode(const void* x, const void* w, int32_t tokens, int32_t rows, int32_t K, int32_t mode,
+                          void* out, int32_t sm_count, int32_t iters, float* ms) {
+  const int bn = nxd::gemm_pick_bn(tokens);
+  CUtensorMap xm;
+  if (!nxd::encode_kmajor(&xm, x, tokens, K, static_cast<uint64_t>(K) * 2, bn))
+    return dfail(NX_ERUNTIME, "tensor map encode failed");
+  __nv_bfloat16* wp = nullptr;
+  int rc = cuda_rc(cudaMalloc(&wp, nxd::packed_weight_elems(rows, K) * 2));
+  if (rc) return rc;
+  rc = cuda_rc(nxd::pack_weights(static_cast<const __nv_bfloat16*>(w), wp, rows, K, nullptr));
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (sm_count <= 0 || sm_count > n_sm) sm_count = n_sm;
+  float* ws = nullptr;
+  const size_t ws_bytes = 256u << 20;
+  if (!rc) rc = cuda_rc(cudaMalloc(&ws, ws_bytes));
+  const int n = iters > 0 ? iters : 1;
+  std::vector<cudaEvent_t> ev(2 * n);
+  for (auto& e : ev) cudaEventCreate(&e);
+  cudaError_t err = rc ? cudaErrorUnknown : cudaSuccess;
+  nxd::GemmFold f;
+  for (int i = 0; i < n && err == cudaSuccess; ++i) {
+    cudaEventRecord(ev[2 * i], nullptr);
+    err = nxd::gemm_decode(wp, xm, bn, rows, tokens, K, static_cast<float*>(out), rows, ws, ws_bytes, sm_count,
+                           nullptr, mode == 16 ? &f : nullptr);
+    cudaEventRecord(ev[2 * i + 1], nullptr);
+  }
+  if (err == cudaSuccess && mode == 16) err = nxd::fold_store_f32(f, static_cast<float*>(out), nullptr);
+  if (err == cudaSuccess) err = cudaDeviceSynchronize();
+  std::vector<float> t(n, 0.f);
+  for (int i = 0; i < n; ++i) cudaEventElapsedTime(&t[i], ev[2 * i], ev[2 * i + 1]);
+  std::sort(t.begin(), t.end());
+  if (ms) *ms = t[n / 2] * n;
+  for (auto& e : ev) cudaEventDestroy(e);
+  cudaFree(ws);
+  cudaFree(wp);
+  return rc ? rc : cuda_rc(err);
+}
+
 int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32_t K, int32_t mode,
                void* out, int32_t ldo, const void* bias, const void* residual, int32_t ldr,
                int32_t sm_count, int32_t splits, int32_t iters, float* ms) {
   return dguard([&] {
+    if (mode == 16 || mode == 17) return op_gemm_decode(x, w, tokens, rows, K, mode, out, sm_count, iters, ms);
     const int bn = nxd::gemm_pick_bn(tokens);
     CUtensorMap xm;
     if (!nxd::encode_kmajor(&xm, x, tokens, K, static_cast<uint64_t>(K) * 2, bn))

@@ -130,6 +130,15 @@ cudaError_t gemm(const __nv_bfloat16* w_packed, const CUtensorMap& x_map, int bn
 // stream-K pieces may wait for each other (parallel fix-up); otherwise the
 // last arriving piece folds the tile alone.
 constexpr size_t gemm_counter_bytes() { return 64 * 1024; }
+// Decode-shaped GEMM (tokens <= 128; gemm_decode.cu): tokens are the MMA's
+// M = 128 side and 256 weight rows its N side (the tensor floor for small
+// token counts). fold != nullptr: fp32 planes for a fold_* consumer (ws as
+// for gemm()); otherwise fp32 out[t * ldo + f] (lm_head logits). x_map's
+// box must hold box_rows <= 128 token rows.
+cudaError_t gemm_decode(const __nv_bfloat16* w_packed, const CUtensorMap& x_map, int box_rows, int rows,
+                        int tokens, int K, float* out, int ldo, float* ws, size_t ws_bytes, int sm_count,
+                        cudaStream_t stream, GemmFold* fold);
+void prepare_gemm_decode_kernel();
 constexpr int kGemmMaxCounterTiles = 8192;  // [arrive | depart] int counters
 
 // K-major bf16 [rows, cols] tensor map with a 64 x box_rows, 128B-swizzled box.
@@ -184,6 +193,8 @@ cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, 
 //  x = bf16(x + sum planes); h = rmsnorm(x) * w (skipped when w == nullptr)
 cudaError_t fold_residual_rmsnorm(const GemmFold& f, __nv_bfloat16* x, const __nv_bfloat16* w, float eps,
                                   __nv_bfloat16* h, cudaStream_t s);
+//  out[t][r] = sum planes (fp32)
+cudaError_t fold_store_f32(const GemmFold& f, float* out, cudaStream_t s);
 //  act[t][64 b + i] = silu(sum gate row 128 b + i) * (sum up row 128 b + 64 + i)
 cudaError_t fold_swiglu(const GemmFold& f, __nv_bfloat16* act, cudaStream_t s);
 //  qkv row = bf16(sum planes + bias), then RoPE + paged KV write as rope_kv_write

@@ -3,6 +3,7 @@
 // TMA descriptor encoder. All loads/stores are 16-byte vectors.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <cudaTypedefs.h>
@@ -155,26 +156,38 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* _
 
 // ---- consumers of deferred-fold GEMM planes ---------------------------------
 // Sum of the fp32 partials of elements [row, row + 8) of token t, in piece
-// order (deterministic for a given partition).
+// order (deterministic for a given partition). The loads of up to 8 pieces
+// are issued before the first add, so a fold costs one L2 round trip, not
+// one per piece.
 __device__ __forceinline__ void fold8(const GemmFold& f, int row, int t, float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = 0.f;
   const int n = fold_pieces(f, row, t);
   const size_t plane = static_cast<size_t>(f.tokens) * f.rows;
   const float* src = f.planes + static_cast<size_t>(t) * f.rows + row;
-  for (int q = 0; q < n; ++q) {
-    const float4 a = __ldcg(reinterpret_cast<const float4*>(src + q * plane));
-    const float4 b = __ldcg(reinterpret_cast<const float4*>(src + q * plane + 4));
-    v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
-    v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+  for (int q0 = 0; q0 < n; q0 += 8) {
+    float4 a[8], b[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q0 + q < n) {
+        a[q] = __ldcg(reinterpret_cast<const float4*>(src + (q0 + q) * plane));
+        b[q] = __ldcg(reinterpret_cast<const float4*>(src + (q0 + q) * plane + 4));
+      }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q0 + q < n) {
+        v[0] += a[q].x, v[1] += a[q].y, v[2] += a[q].z, v[3] += a[q].w;
+        v[4] += b[q].x, v[5] += b[q].y, v[6] += b[q].z, v[7] += b[q].w;
+      }
   }
 }
 
-// One CTA (256 threads) per token; hidden <= 256 * 8 * kFoldVec.
-constexpr int kFoldVec = 4;
-__global__ void __launch_bounds__(256) fold_residual_rmsnorm_kernel(GemmFold f, __nv_bfloat16* __restrict__ x,
-                                                                    const __nv_bfloat16* __restrict__ w, float eps,
-                                                                    __nv_bfloat16* __restrict__ h) {
+// One CTA per token, one 8-feature chunk per thread (blockDim = hidden / 8,
+// <= 512; kFoldVec chunks per thread beyond that).
+constexpr int kFoldVec = 2;
+__global__ void __launch_bounds__(512) fold_residual_rmsnorm_kernel(GemmFold f, __nv_bfloat16* __restrict__ x,
+                                                                     const __nv_bfloat16* __restrict__ w, float eps,
+                                                                     __nv_bfloat16* __restrict__ h) {
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x, d = f.rows;
@@ -183,7 +196,7 @@ __global__ void __launch_bounds__(256) fold_residual_rmsnorm_kernel(GemmFold f, 
   float ss = 0.f;
 #pragma unroll
   for (int c = 0; c < kFoldVec; ++c) {
-    const int row = (threadIdx.x + c * 256) * 8;
+    const int row = (threadIdx.x + c * blockDim.x) * 8;
     if (row >= d) break;
     float v[8];
     fold8(f, row, t, v);
@@ -199,19 +212,18 @@ __global__ void __launch_bounds__(256) fold_residual_rmsnorm_kernel(GemmFold f, 
     *reinterpret_cast<uint4*>(xr + row) = *reinterpret_cast<uint4*>(o);
   }
   if (w == nullptr) return;
-  __shared__ float red[8];
+  __shared__ float red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   float tot = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) tot += red[i];
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += red[i];
   const float inv = rsqrtf(tot / d + eps);
   __nv_bfloat16* hr = h + static_cast<size_t>(t) * d;
 #pragma unroll
   for (int c = 0; c < kFoldVec; ++c) {
-    const int row = (threadIdx.x + c * 256) * 8;
+    const int row = (threadIdx.x + c * blockDim.x) * 8;
     if (row >= d) break;
     const uint4 wv = *reinterpret_cast<const uint4*>(w + row);
     const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(&wv);
@@ -220,6 +232,20 @@ __global__ void __launch_bounds__(256) fold_residual_rmsnorm_kernel(GemmFold f, 
     for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(keep[c][i] * inv * __bfloat162float(wb[i]));
     *reinterpret_cast<uint4*>(hr + row) = *reinterpret_cast<uint4*>(o);
   }
+}
+
+// out[t][r] = sum planes (fp32): the plain fold (tests, diagnostics).
+__global__ void __launch_bounds__(256) fold_store_f32_kernel(GemmFold f, float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.y;
+  const int row = (blockIdx.x * 256 + threadIdx.x) * 8;
+  if (row >= f.rows) return;
+  float v[8];
+  fold8(f, row, t, v);
+  float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(t) * f.rows + row);
+  dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+  dst[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
@@ -234,7 +260,7 @@ __global__ void __launch_bounds__(256) fold_swiglu_kernel(GemmFold f, __nv_bfloa
   if (j >= ffn) return;
   const int rg = (j >> 6) * 128 + (j & 63);  // gate rows of 128-row block j / 64; up = +64
   float g[8], u[8];
-  fold8(f, rg, t, g);
+  fold8(f, rg, t, g);  // the g and u loads are independent: both in flight
   fold8(f, rg + 64, t, u);
   __align__(16) __nv_bfloat16 o[8];
 #pragma unroll
@@ -245,7 +271,7 @@ __global__ void __launch_bounds__(256) fold_swiglu_kernel(GemmFold f, __nv_bfloa
 // One CTA per token: the qkv row is folded into shared memory (+ bias,
 // rounded to bf16 exactly like the GEMM's bias/store epilogue), then RoPE
 // and the paged KV write run on it.
-__global__ void __launch_bounds__(256) fold_rope_kv_kernel(GemmFold f, const __nv_bfloat16* __restrict__ bias,
+__global__ void __launch_bounds__(512) fold_rope_kv_kernel(GemmFold f, const __nv_bfloat16* __restrict__ bias,
                                                            __nv_bfloat16* __restrict__ qkv,
                                                            const int32_t* __restrict__ slot,
                                                            const float2* __restrict__ table, int n_heads,
@@ -427,9 +453,17 @@ cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, 
 cudaError_t fold_residual_rmsnorm(const GemmFold& f, __nv_bfloat16* x, const __nv_bfloat16* w, float eps,
                                   __nv_bfloat16* h, cudaStream_t s) {
   if (f.tokens == 0) return cudaSuccess;
-  if (f.rows % 8 || f.rows > 256 * 8 * kFoldVec) return cudaErrorInvalidValue;
+  if (f.rows % 256 || f.rows > 512 * 8 * kFoldVec) return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  return launch_pdl(fold_residual_rmsnorm_kernel, dim3(f.tokens), dim3(256), 0, s, f, x, w, eps, h);
+  return launch_pdl(fold_residual_rmsnorm_kernel, dim3(f.tokens), dim3(std::min(512, f.rows / 8)), 0, s, f, x, w,
+                    eps, h);
+}
+
+cudaError_t fold_store_f32(const GemmFold& f, float* out, cudaStream_t s) {
+  if (f.tokens == 0) return cudaSuccess;
+  if (f.rows % 8) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  return launch_pdl(fold_store_f32_kernel, dim3((f.rows + 2047) / 2048, f.tokens), dim3(256), 0, s, f, out);
 }
 
 cudaError_t fold_swiglu(const GemmFold& f, __nv_bfloat16* act, cudaStream_t s) {
@@ -446,7 +480,8 @@ cudaError_t fold_rope_kv(const GemmFold& f, const __nv_bfloat16* bias, __nv_bflo
   if (f.tokens == 0) return cudaSuccess;
   if (f.rows != (n_heads + 2 * n_kv_heads) * 128) return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  return launch_pdl(fold_rope_kv_kernel, dim3(f.tokens), dim3(256), static_cast<size_t>(f.rows) * 2, s, f, bias,
+  return launch_pdl(fold_rope_kv_kernel, dim3(f.tokens), dim3(std::min(512, f.rows / 8)),
+                    static_cast<size_t>(f.rows) * 2, s, f, bias,
                     qkv, slot, table, n_heads, n_kv_heads, page_tokens, kplane, vplane);
 }
 
@@ -525,6 +560,7 @@ void ensure_kernels_prepared() {
   std::lock_guard<std::mutex> lk(mu);
   if (mask.load() & bit) return;
   prepare_gemm_kernels();
+  prepare_gemm_decode_kernel();
   prepare_attention_kernels();
   prepare_tp_kernels();
   const void* fns[] = {reinterpret_cast<const void*>(fill_random_kernel),
@@ -535,6 +571,7 @@ void ensure_kernels_prepared() {
                        reinterpret_cast<const void*>(rope_kv_kernel),
                        reinterpret_cast<const void*>(fold_residual_rmsnorm_kernel),
                        reinterpret_cast<const void*>(fold_swiglu_kernel),
+                       reinterpret_cast<const void*>(fold_store_f32_kernel),
                        reinterpret_cast<const void*>(fold_rope_kv_kernel),
                        reinterpret_cast<const void*>(argmax_partial_kernel),
                        reinterpret_cast<const void*>(argmax_final_kernel),

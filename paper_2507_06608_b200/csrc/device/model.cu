@@ -558,9 +558,9 @@ void Model::forward(LaneWs& ws) {
         ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
       });
     timed(gk, gbytes(qkv_rows_, d, fold ? 4 : 2, false), gflops(qkv_rows_, d), [&] {
-      ck(gemm(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
-              ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive,
-              fold ? &fq : nullptr),
+      ck(fold ? gemm_decode(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fq)
+              : gemm(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
+                     ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "qkv gemm");
     });
     if (fold)
@@ -594,8 +594,9 @@ void Model::forward(LaneWs& ws) {
     // their partial; the all-reduce then yields x + sum_r o_r on every rank.
     const int res_mode = (tp_ == 1 || rank_ == 0) ? kEpiResidual : kEpiStore;
     timed(gk, gbytes(d, attn_cols_, fold ? 4 : 2, !fold), gflops(d, attn_cols_), [&] {
-      ck(gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x,
-              d, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive, fold ? &fo : nullptr),
+      ck(fold ? gemm_decode(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fo)
+              : gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x,
+                     d, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "o gemm");
     });
     if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
@@ -608,8 +609,9 @@ void Model::forward(LaneWs& ws) {
         ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
       });
     timed(gk, gbytes(2.0 * ffn_, d, fold ? 8 : 1, false), gflops(2.0 * ffn_, d), [&] {
-      ck(gemm(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr,
-              nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive, fold ? &fg : nullptr),
+      ck(fold ? gemm_decode(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fg)
+              : gemm(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr,
+                     nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "gate/up gemm");
     });
     if (fold)
@@ -617,8 +619,9 @@ void Model::forward(LaneWs& ws) {
         ck(fold_swiglu(fg, ws.act, s), "fold swiglu");
       });
     timed(gk, gbytes(d, ffn_, fold ? 4 : 2, !fold), gflops(d, ffn_), [&] {
-      ck(gemm(w.down, ws.map_act[bi], bn, d, T, ffn_, res_mode, ws.x, d, nullptr, ws.x, d,
-              ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive, fold ? &fd : nullptr),
+      ck(fold ? gemm_decode(w.down, ws.map_act[bi], bn, d, T, ffn_, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fd)
+              : gemm(w.down, ws.map_act[bi], bn, d, T, ffn_, res_mode, ws.x, d, nullptr, ws.x, d,
+                     ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "down gemm");
     });
     if (tp_ > 1) timed(NX_K_OTHER, Td * d * 2 * 2, 0, [&] { all_reduce(ws, ws.x, static_cast<size_t>(T) * d); });
@@ -641,8 +644,11 @@ void Model::forward(LaneWs& ws) {
     const int sbn = gemm_pick_bn(n);
     timed(gk, static_cast<double>(vocab_l_) * d * 2 + nd * d * 2 + nd * vocab_l_ * 4,
           2.0 * nd * vocab_l_ * d, [&] {
-            ck(gemm(lm_head_, ws.map_hs[bn_index(sbn)], sbn, vocab_l_, n, d, kEpiF32, ws.logits,
-                    vocab_l_, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
+            ck(fold && n <= 128
+                   ? gemm_decode(lm_head_, ws.map_hs[bn_index(sbn)], sbn, vocab_l_, n, d, ws.logits, vocab_l_,
+                                 ws.ws, ws.ws_bytes, sm, s, nullptr)
+                   : gemm(lm_head_, ws.map_hs[bn_index(sbn)], sbn, vocab_l_, n, d, kEpiF32, ws.logits,
+                          vocab_l_, nullptr, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
                "lm_head gemm");
           });
     timed(NX_K_OTHER, nd * vocab_l_ * 4, 0, [&] {

@@ -236,6 +236,8 @@ class Buf:
 
 
 EPI_STORE, EPI_BIAS, EPI_RESIDUAL, EPI_BIAS_RESIDUAL, EPI_SWIGLU, EPI_F32 = 0, 1, 2, 3, 4, 6
+EPI_DECODE_FOLD = 16  # decode GEMM (tokens <= 128): stream-K fold planes -> fp32 out
+EPI_DECODE_F32 = 17   # decode GEMM, direct fp32 out (data-parallel)
 
 
 def gemm(x: Buf, w: Buf, tokens: int, rows: int, K: int, mode: int, out: Buf, ldo: int,

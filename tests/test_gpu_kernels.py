@@ -81,6 +81,22 @@ def test_gemm_swiglu(D, T, splits):
     _close(D.bf16_to_f32(bo.to_array((T, F), np.uint16)), ref)
 
 
+@pytest.mark.parametrize("T,N,K,sms", [(1, 1024, 512, 0), (37, 4096 + 128, 4096, 0), (64, 4096, 4096, 48),
+                                       (128, 6144, 4096, 16), (64, 4096, 14336, 148), (100, 28672, 4096, 0)])
+def test_gemm_decode(D, T, N, K, sms):
+    """Decode GEMM (tokens = MMA M, 256 weight rows = N): stream-K fold planes
+    summed by the fold kernel, and the direct fp32 (data-parallel) form."""
+    rng = np.random.default_rng(T + N)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    ref = D.bf16_to_f32(x) @ D.bf16_to_f32(w).T
+    bx, bw = D.Buf.from_array(x), D.Buf.from_array(w)
+    for mode in (D.EPI_DECODE_FOLD, D.EPI_DECODE_F32):
+        bo = D.Buf(T * N * 4)
+        D.gemm(bx, bw, T, N, K, mode, bo, N, sm_count=sms)
+        dev = bo.to_array((T, N), np.float32)
+        np.testing.assert_allclose(dev, ref, rtol=1e-3, atol=1e-3 * np.abs(ref).max())
+
+
 def test_gemm_f32_logits(D):
     T, N, K = 40, 1024 * 8, 512
     rng = np.random.default_rng(9)
