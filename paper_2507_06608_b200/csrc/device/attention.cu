@@ -58,6 +58,12 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// 8x8 b16 transpose across the warp (fragment layout in and out).
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t v) {
+  uint32_t r;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -301,9 +307,8 @@ __global__ void __launch_bounds__(kThreadsAttn)
 // boundaries so the pipeline never drains. An item covered by one warp is
 // finalized in place; an item split across warps leaves (m, l, O) partials
 // that decode_combine_kernel folds with a log-sum-exp rescale.
-// The G <= 8 query heads of a kv head are the MMA rows (m16n8k16, rows >= G
-// zero); only accumulator rows 0..7 are live, so the softmax touches half of
-// the fragment.
+// The tile math is transposed (keys / head dims on the MMA's M side, the
+// G <= 8 query heads of the kv head on its N = 8 side; see the kernel).
 constexpr int kKTD = 32;      // keys per decode tile (two 16-token pages)
 constexpr int kStD = 3;       // ring stages per warp
 constexpr int kWarpsD = 4;    // warps per CTA (one CTA per SM)
@@ -403,18 +408,23 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
     }
   }
   DecPos cur = dec_locate(seq_prefix, n_seq, hkv, lo);
-  uint32_t qf[8][4];
-  float m = -INFINITY, l = 0.f;  // row lane / 4 (rows 8..15 are padding)
-  float o[16][2];
+  // Transposed tile math: S^T = K Q^T and O^T += V^T P^T, so keys / head
+  // dims are the MMA's 16-row M side and the <= 8 query heads of the GQA
+  // group its N = 8 side (half the m16n8k16 count of Q-as-rows, where 16 MMA
+  // rows carry G = 4 heads). Lane l owns heads h0 = 2 (l & 3), h0 + 1.
+  uint32_t qb[8][2];   // B fragments of Q^T, 8 k-steps of 16 dims
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  float o[8][4];       // O^T block db: dims 16 db + l/4 (+8) x heads h0, h0 + 1
   AttnSeq meta = seqs[cur.seq];
   int seg_tile0 = cur.tile;
+  const int h0 = 2 * (lane & 3);
   for (long long gt = lo; gt < hi; ++gt) {
     const int i = static_cast<int>(gt - lo), buf = i % kStD;
     if (gt == lo || cur.tile == 0) {  // new segment: this item's queries
       __syncwarp();
       meta = seqs[cur.seq];
       seg_tile0 = cur.tile;
-      for (int c = lane; c < 16 * 16; c += 32) {
+      for (int c = lane; c < 8 * 16; c += 32) {
         const int r = c >> 4, chunk = c & 15;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (r < g.group)
@@ -424,76 +434,74 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
       }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int row = (lane & 7) + (((lane >> 3) & 1) << 3);
-        const int col = k * 16 + ((lane >> 4) << 3);
-        ldsm_x4(qf[k], sq + swz(row, col));
+      for (int k = 0; k < 8; k += 2) {
+        uint32_t r[4];
+        ldsm_x4(r, sq + swz(lane & 7, k * 16 + ((lane >> 3) << 3)));
+        qb[k][0] = r[0], qb[k][1] = r[1], qb[k + 1][0] = r[2], qb[k + 1][1] = r[3];
       }
-      m = -INFINITY;
-      l = 0.f;
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
 #pragma unroll
-      for (int d = 0; d < 16; ++d) o[d][0] = o[d][1] = 0.f;
+      for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     }
     mbar_wait(&full[buf], (i / kStD) & 1);
     const __nv_bfloat16* sk = wbase + buf * 2 * kTileD;
     const __nv_bfloat16* sv = sk + kTileD;
-    // S = Q K^T: 4 blocks of 8 keys, 8 k-steps each (4 independent chains)
-    float s[4][4];
+    // S^T = K Q^T: 2 blocks of 16 keys x 8 k-steps
+    float s[2][4];
 #pragma unroll
-    for (int n = 0; n < 4; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+    for (int mb = 0; mb < 2; ++mb) s[mb][0] = s[mb][1] = s[mb][2] = s[mb][3] = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
-      for (int n2 = 0; n2 < 2; ++n2) {
-        uint32_t b[4];
-        const int row = n2 * 16 + (lane & 7) + ((lane >> 4) << 3);
-        const int col = k * 16 + (((lane >> 3) & 1) << 3);
-        ldsm_x4(b, sk + swz(row, col));
-        mma16816(s[2 * n2], qf[k], b[0], b[1]);
-        mma16816(s[2 * n2 + 1], qf[k], b[2], b[3]);
+      for (int mb = 0; mb < 2; ++mb) {
+        uint32_t a[4];
+        ldsm_x4(a, sk + swz(mb * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), k * 16 + ((lane >> 4) << 3)));
+        mma16816(s[mb], a, qb[k][0], qb[k][1]);
       }
-    // mask keys past kv_len, online softmax on the live row (c0, c1)
-    const int key0 = cur.tile * kKTD;
-    float mx = m;
+    // mask keys past kv_len; online softmax down each head column
+    const int key0 = cur.tile * kKTD + (lane >> 2);
+    float mx0 = m0, mx1 = m1;
 #pragma unroll
-    for (int n = 0; n < 4; ++n)
+    for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int key = key0 + n * 8 + (lane & 3) * 2 + j;
-        s[n][j] = key < meta.kv_len ? s[n][j] * g.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s[n][j]);
+        const bool ok = key0 + mb * 16 + j * 8 < meta.kv_len;
+        s[mb][2 * j] = ok ? s[mb][2 * j] * g.scale_log2 : -INFINITY;
+        s[mb][2 * j + 1] = ok ? s[mb][2 * j + 1] * g.scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, s[mb][2 * j]);
+        mx1 = fmaxf(mx1, s[mb][2 * j + 1]);
       }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, 2));
-    const float base = mx == -INFINITY ? 0.f : mx;
-    const float alpha = exp2f(m - base);
-    m = mx;
-    l *= alpha;
 #pragma unroll
-    for (int d = 0; d < 16; ++d) o[d][0] *= alpha, o[d][1] *= alpha;
-    uint32_t pf[2][4];
-#pragma unroll
-    for (int n = 0; n < 4; ++n) {
-      const float p0 = exp2f(s[n][0] - base), p1 = exp2f(s[n][1] - base);
-      l += p0 + p1;
-      pf[n >> 1][(n & 1) ? 2 : 0] = pack_bf16(p0, p1);
-      pf[n >> 1][(n & 1) ? 3 : 1] = 0u;  // rows 8..15: padding
+    for (int x = 4; x < 32; x <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, x));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, x));
     }
-    // O += P V (16 output blocks of 8 dims, 2 k-steps of 16 keys)
+    const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
+    const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
+    m0 = mx0, m1 = mx1;
+    l0 *= al0, l1 *= al1;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) o[d][0] *= al0, o[d][2] *= al0, o[d][1] *= al1, o[d][3] *= al1;
+    // P^T in C layout (keys x heads) -> B fragments (keys = k) by an 8x8 transpose
+    uint32_t pb[2][2];
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb) {
+      const float p00 = exp2f(s[mb][0] - b0), p01 = exp2f(s[mb][1] - b1);
+      const float p10 = exp2f(s[mb][2] - b0), p11 = exp2f(s[mb][3] - b1);
+      l0 += p00 + p10;
+      l1 += p01 + p11;
+      pb[mb][0] = movmatrix_trans(pack_bf16(p00, p01));
+      pb[mb][1] = movmatrix_trans(pack_bf16(p10, p11));
+    }
+    // O^T += V^T P^T: 8 blocks of 16 dims x 2 k-steps of 16 keys
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-      for (int d2 = 0; d2 < 8; ++d2) {
-        uint32_t b[4];
-        const int row = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
-        const int col = d2 * 16 + ((lane >> 4) << 3);
-        ldsm_x4_t(b, sv + swz(row, col));
-        float c0[4] = {o[2 * d2][0], o[2 * d2][1], 0.f, 0.f};
-        float c1[4] = {o[2 * d2 + 1][0], o[2 * d2 + 1][1], 0.f, 0.f};
-        mma16816(c0, pf[ks], b[0], b[1]);
-        mma16816(c1, pf[ks], b[2], b[3]);
-        o[2 * d2][0] = c0[0], o[2 * d2][1] = c0[1];
-        o[2 * d2 + 1][0] = c1[0], o[2 * d2 + 1][1] = c1[1];
+      for (int db = 0; db < 8; ++db) {
+        uint32_t a[4];
+        ldsm_x4_t(a, sv + swz(ks * 16 + (lane & 7) + ((lane >> 4) << 3), db * 16 + (((lane >> 3) & 1) << 3)));
+        mma16816(o[db], a, pb[ks][0], pb[ks][1]);
       }
     __syncwarp();
     // refill this stage kStD tiles ahead
@@ -507,37 +515,54 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
     // segment end: last tile of the item or of this warp's range
     const bool item_end = cur.tile == cur.n_tiles - 1;
     if (item_end || gt == hi - 1) {
-      float lt = l;
-      lt += __shfl_xor_sync(0xffffffff, lt, 1);
-      lt += __shfl_xor_sync(0xffffffff, lt, 2);
-      const int r = lane >> 2;
+      float lt0 = l0, lt1 = l1;
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1) {
+        lt0 += __shfl_xor_sync(0xffffffff, lt0, x);
+        lt1 += __shfl_xor_sync(0xffffffff, lt1, x);
+      }
       const bool whole = seg_tile0 == 0 && item_end;
-      if (r < g.group) {
-        const int head = cur.kvh * g.group + r;
-        if (whole) {
-          const float inv = lt > 0.f ? 1.f / lt : 0.f;
-          __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + head * kHD;
+      const float sc0 = whole ? (lt0 > 0.f ? 1.f / lt0 : 0.f) : 1.f;
+      const float sc1 = whole ? (lt1 > 0.f ? 1.f / lt1 : 0.f) : 1.f;
+      // stage [8 heads][128 dims] in the (free) Q area, then coalesced stores
+      float* so = reinterpret_cast<float*>(sq);
+      __syncwarp();
 #pragma unroll
-          for (int d = 0; d < 16; ++d) {
-            const int col = d * 8 + (lane & 3) * 2;
-            *reinterpret_cast<uint32_t*>(dst + col) = pack_bf16(o[d][0] * inv, o[d][1] * inv);
+      for (int d = 0; d < 8; ++d) {
+        const int dim = d * 16 + (lane >> 2);
+        so[h0 * kHD + dim] = o[d][0] * sc0;
+        so[(h0 + 1) * kHD + dim] = o[d][1] * sc1;
+        so[h0 * kHD + dim + 8] = o[d][2] * sc0;
+        so[(h0 + 1) * kHD + dim + 8] = o[d][3] * sc1;
+      }
+      __syncwarp();
+      if (whole) {
+        __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + cur.kvh * g.group * kHD;
+        for (int c = lane; c < g.group * 16; c += 32) {
+          const float4 u = *reinterpret_cast<const float4*>(so + c * 8);
+          const float4 v = *reinterpret_cast<const float4*>(so + c * 8 + 4);
+          uint4 w;
+          w.x = pack_bf16(u.x, u.y), w.y = pack_bf16(u.z, u.w), w.z = pack_bf16(v.x, v.y), w.w = pack_bf16(v.z, v.w);
+          *reinterpret_cast<uint4*>(dst + c * 8) = w;
+        }
+      } else {
+        // piece index of this warp within the item (stream-K ownership rule)
+        const long long first = ((cur.item_start + 1) * W - 1) / total;
+        const size_t slot = (static_cast<size_t>(cur.seq) * hkv + cur.kvh) * max_pieces + (gw - first);
+        float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
+        for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(so + c * 4);
+        if (lane < 4) {
+          if (h0 < g.group) {
+            part_ml[(slot * g.group + h0) * 2] = m0;
+            part_ml[(slot * g.group + h0) * 2 + 1] = lt0;
           }
-        } else {
-          // piece index of this warp within the item (stream-K ownership rule)
-          const long long first = ((cur.item_start + 1) * W - 1) / total;
-          const size_t slot = (static_cast<size_t>(cur.seq) * hkv + cur.kvh) * max_pieces + (gw - first);
-          float* po = part_o + (slot * g.group + r) * kHD;
-#pragma unroll
-          for (int d = 0; d < 16; ++d) {
-            const int col = d * 8 + (lane & 3) * 2;
-            *reinterpret_cast<float2*>(po + col) = make_float2(o[d][0], o[d][1]);
-          }
-          if ((lane & 3) == 0) {
-            part_ml[(slot * g.group + r) * 2] = m;
-            part_ml[(slot * g.group + r) * 2 + 1] = lt;
+          if (h0 + 1 < g.group) {
+            part_ml[(slot * g.group + h0 + 1) * 2] = m1;
+            part_ml[(slot * g.group + h0 + 1) * 2 + 1] = lt1;
           }
         }
       }
+      __syncwarp();
     }
     dec_advance(cur, seq_prefix, n_seq, hkv);
   }

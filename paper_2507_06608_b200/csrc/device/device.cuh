@@ -76,6 +76,7 @@ struct GemmParams {
   int coresident;  // stream-K: parallel reduce-scatter fix-up (see gemm())
   int dbg;         // experiments only (NX_GEMM_DBG): 1 skip X loads, 2 skip MMAs
   int fold;        // 1: every work item writes fp32 planes, no fix-up (see GemmFold)
+  int sk_tile0;    // stream-K covers tiles [sk_tile0, tiles); earlier tiles run data-parallel
 };
 
 int gemm_pick_bn(int tokens);

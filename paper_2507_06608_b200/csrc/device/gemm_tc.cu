@@ -129,6 +129,16 @@ struct Work {
   bool partial;  // true: write fp32 partials for a fix-up pass
 };
 
+// Stream-K covers tiles [p.sk_tile0, tiles): the leading tiles (whole
+// waves) run data-parallel first (hybrid schedule for prefill shapes). Counter,
+// slot and piece arithmetic use the stream-K-local tile index.
+__device__ __forceinline__ int sk_local(const GemmParams& p, int m_blk, int n_blk) {
+  return m_blk * p.n_nblk + n_blk - p.sk_tile0;
+}
+__device__ __forceinline__ long long sk_total(const GemmParams& p) {
+  return (static_cast<long long>(p.n_mblk) * p.n_nblk - p.sk_tile0) * p.num_kb;
+}
+
 // This CTA's work items, in the same order for every warp role.
 //  * data-parallel / split-K: units blockIdx.x, +gridDim.x, ...
 //  * stream-K: the contiguous iteration range [c*I/G, (c+1)*I/G) over the
@@ -138,22 +148,32 @@ struct WorkIter {
   int u = 0;
   long long it = 0, end = 0, total = 0;
   __device__ explicit WorkIter(const GemmParams& pp) : p(pp) {
+    u = blockIdx.x;
     if (p.streamk) {
-      total = static_cast<long long>(p.n_mblk) * p.n_nblk * p.num_kb;
+      total = sk_total(p);
       it = total * blockIdx.x / gridDim.x;
       end = total * (blockIdx.x + 1) / gridDim.x;
-    } else {
-      u = blockIdx.x;
     }
   }
   __device__ bool next(Work& w) {
+    if (p.streamk && u < p.sk_tile0) {  // hybrid: whole-tile waves first
+      w.n_blk = u % p.n_nblk;
+      w.m_blk = u / p.n_nblk;
+      w.kb0 = 0;
+      w.kb1 = p.num_kb;
+      w.partial = false;
+      w.slot = -1;
+      w.piece = 0;
+      u += gridDim.x;
+      return true;
+    }
     if (p.streamk) {
       if (it >= end) return false;
-      const int tile = static_cast<int>(it / p.num_kb);
+      const int tile = static_cast<int>(it / p.num_kb);  // stream-K-local
       w.kb0 = static_cast<int>(it % p.num_kb);
       w.kb1 = static_cast<int>(min(static_cast<long long>(p.num_kb), w.kb0 + (end - it)));
-      w.n_blk = tile % p.n_nblk;
-      w.m_blk = tile / p.n_nblk;
+      w.n_blk = (tile + p.sk_tile0) % p.n_nblk;
+      w.m_blk = (tile + p.sk_tile0) / p.n_nblk;
       w.partial = !(w.kb0 == 0 && w.kb1 == p.num_kb);
       w.slot = -1;
       w.piece = 0;
@@ -186,8 +206,8 @@ struct WorkIter {
 // applies the epilogue (classic threadfence reduction; no extra launch).
 template <int BN, int MT>
 __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& w, int et, int* s_flag) {
-  const int tile = w.m_blk * p.n_nblk + w.n_blk;
-  const long long total = static_cast<long long>(p.n_mblk) * p.n_nblk * p.num_kb;
+  const int tile = sk_local(p, w.m_blk, w.n_blk);
+  const long long total = sk_total(p);
   const long long it0 = static_cast<long long>(tile) * p.num_kb;
   const int first = static_cast<int>(((it0 + 1) * gridDim.x - 1) / total);
   const int last = static_cast<int>(((it0 + p.num_kb) * gridDim.x - 1) / total);
@@ -292,7 +312,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 }
 
 __device__ __forceinline__ void streamk_tile_pieces(const GemmParams& p, int tile, int* first, int* pieces) {
-  const long long total = static_cast<long long>(p.n_mblk) * p.n_nblk * p.num_kb;
+  const long long total = sk_total(p);
   const long long it0 = static_cast<long long>(tile) * p.num_kb;
   *first = static_cast<int>(((it0 + 1) * gridDim.x - 1) / total);
   const int last = static_cast<int>(((it0 + p.num_kb) * gridDim.x - 1) / total);
@@ -327,13 +347,13 @@ template <int BN, int MT>
 __device__ void streamk_publish(const GemmParams& p, const Work& w, int et) {
   __threadfence();
   named_bar_sync(1, kEpiThreads);
-  if (et == 0) atomicAdd(&p.tile_count[w.m_blk * p.n_nblk + w.n_blk], 1);
+  if (et == 0) atomicAdd(&p.tile_count[sk_local(p, w.m_blk, w.n_blk)], 1);
 }
 
 template <int BN, int MT>
 __device__ void streamk_reduce_slice(const GemmParams& p, int m_blk, int n_blk, int et, uint8_t* scratch,
                                      uint64_t* bar, uint32_t& phase) {
-  const int tile = m_blk * p.n_nblk + n_blk;
+  const int tile = sk_local(p, m_blk, n_blk);
   int first, pieces;
   streamk_tile_pieces(p, tile, &first, &pieces);
   const int piece = static_cast<int>(blockIdx.x) - first;
@@ -766,6 +786,16 @@ cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const Gemm
 
 }  // namespace
 
+// Prefill hybrid stream-K applies when the last wave is at most this full
+// (NX_HYBRID_FRAC; 0 disables).
+static double hybrid_max_frac() {
+  static const double f = [] {
+    const char* e = std::getenv("NX_HYBRID_FRAC");
+    return e ? std::atof(e) : 0.85;
+  }();
+  return f;
+}
+
 size_t packed_weight_elems(int rows, int K) {
   const int blocks = (rows + kBM - 1) / kBM;
   return static_cast<size_t>((blocks + 1) & ~1) * kBM * K;
@@ -902,6 +932,20 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
       grid = G;
     } else {
       grid = std::max(1, std::min(tiles, sm_count));
+    }
+  } else if (tokens > 256 && ws != nullptr && tiles > sm_count && tiles % sm_count != 0 &&
+             static_cast<double>(tiles % sm_count) / sm_count < hybrid_max_frac()) {
+    // Hybrid: whole waves data-parallel, the partial last wave stream-K
+    // (e.g. o / down at T = 2048 on 112 SMs: 256 tiles = 2.29 waves, not 3).
+    const int rem = tiles % sm_count;
+    const long long rem_iters = static_cast<long long>(rem) * p.num_kb;
+    const long long per_min = std::max<long long>(1, rem_iters / sm_count);
+    p.max_pieces = static_cast<int>((p.num_kb + per_min - 1) / per_min) + 1;
+    const size_t need = static_cast<size_t>(rem) * p.max_pieces * mt * bn * kBM * 4;
+    grid = sm_count;
+    if (need <= ws_bytes && rem <= kGemmMaxCounterTiles) {
+      p.streamk = 1;
+      p.sk_tile0 = tiles - rem;
     }
   } else {
     grid = std::max(1, std::min(tiles, sm_count));

@@ -51,6 +51,19 @@ def test_gemm_splits_and_small_grids(D, T, N, K, splits, sms):
     _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), ref)
 
 
+@pytest.mark.parametrize("T,N,K,sms", [(1024, 4096, 1024, 112), (2048, 6144, 512, 148), (700, 4096, 512, 40)])
+def test_gemm_prefill_hybrid_streamk(D, T, N, K, sms):
+    """Prefill shapes whose last wave is partial: whole waves data-parallel,
+    the remainder stream-K with the in-kernel fix-up (residual epilogue)."""
+    rng = np.random.default_rng(T + sms)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    r = _rand(D, rng, (T, N))
+    ref = D.bf16_to_f32(x) @ D.bf16_to_f32(w).T + D.bf16_to_f32(r)
+    bx, bw, br, bo = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf.from_array(r), D.Buf(T * N * 2)
+    D.gemm(bx, bw, T, N, K, D.EPI_RESIDUAL, bo, N, residual=br, ldr=N, sm_count=sms)
+    _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), ref)
+
+
 @pytest.mark.parametrize("T,splits", [(9, 1), (64, 4), (500, 1)])
 def test_gemm_bias_residual(D, T, splits):
     N, K = 1024, 1024
