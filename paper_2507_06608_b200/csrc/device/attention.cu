@@ -1,11 +1,14 @@
 // Paged attention over the device-resident block table.
 //
-// KV cache layout per layer: K and V planes of [page][kv_head][16][hd] bf16,
-// written pre-swizzled (16 B chunk c of token row r stored at c ^ (r & 7)), so
-// one (page, kv head) is a contiguous 4 KB run that is *already* the
-// conflict-free shared-memory image: a 64-key tile is 4 + 4 cp.async.bulk
-// copies issued by one thread on an mbarrier, with no per-thread address math
-// (the 16 B-per-thread loader this replaced was instruction-bound at ~2 TB/s).
+// KV cache layout per layer: [page][kv_head][K | V][16][hd] bf16, written
+// pre-swizzled (16 B chunk c of token row r stored at c ^ (r & 7)), so one
+// (page, kv head) is a contiguous 8 KB run [K 16 x 128 | V 16 x 128] that is
+// *already* the conflict-free shared-memory image: a 64-key tile is 4
+// cp.async.bulk copies issued by one thread on an mbarrier. In smem, key r of
+// a tile sits at row kv_row(r) = 32 (r / 16) + r % 16 of the K view and the
+// same row of the V view (16 rows further). One 8 KB copy instead of two 4 KB
+// ones: bulk copies pay a per-copy cost (tools/bw_probe.cu: 4 KB copies 27-55
+// GB/s/SM, 16-32 KB copies 107-190 GB/s/SM).
 //
 //  * prefill: CTA = (sequence, kv head, 64 query rows); a query row is a
 //    (token, head-in-GQA-group) pair so all G heads sharing a KV head reuse
@@ -34,6 +37,10 @@ constexpr int kKT = 64;         // keys per staged tile
 constexpr int kRowsPF = 64;     // query rows per prefill CTA
 constexpr int kThreadsAttn = 128;
 constexpr int kStagesPF = 2;   // prefill: 2 x 32 KB KV stages (+16 KB Q staging)
+
+constexpr int kKVBlock = 2 * 16 * kHD;  // elements of one (page, kv head) K|V block
+// Smem row of key r of a tile of interleaved (page, kv head) blocks.
+__device__ __forceinline__ int kv_row(int r) { return ((r >> 4) << 5) | (r & 15); }
 
 // Swizzled offset (elements) of (row, col) in a [rows][128] bf16 tile.
 __device__ __forceinline__ int swz(int row, int col) {
@@ -85,9 +92,8 @@ __device__ __forceinline__ void issue_kv_tile(__nv_bfloat16* sk, __nv_bfloat16* 
   for (int p = 0; p < 4; ++p) {
     const int key = key0 + p * 16;
     const int page = key < kv_end ? pages[key >> 4] : last_page;
-    const size_t off = (static_cast<size_t>(page) * g.n_kv_heads + kvh) * (16 * kHD);
-    bulk_load(sk + p * 16 * kHD, kplane + off, 4096, bar, policy);
-    bulk_load(sv + p * 16 * kHD, vplane + off, 4096, bar, policy);
+    const size_t off = (static_cast<size_t>(page) * g.n_kv_heads + kvh) * kKVBlock;
+    bulk_load(sk + p * kKVBlock, kplane + off, 8192, bar, policy);  // sv = sk + 16 rows
   }
 }
 
@@ -113,7 +119,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       uint32_t b[4];
-      const int row = kb + (lane & 7) + ((lane >> 4) << 3);
+      const int row = kv_row(kb + (lane & 7) + ((lane >> 4) << 3));
       const int col = k * 16 + (((lane >> 3) & 1) << 3);
       ldsm_x4(b, sk + swz(row, col));
       mma16816(s[2 * n2], qf[k], b[0], b[1]);
@@ -139,20 +145,24 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __
     mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 1));
     mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 2));
   }
-  float alpha[2], base[2];
+  float base[2];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    base[r] = mx[r] == -INFINITY ? 0.f : mx[r];
-    alpha[r] = exp2f(m[r] - base[r]);
-    m[r] = mx[r];
-    l[r] *= alpha[r];
-  }
+  for (int r = 0; r < 2; ++r) base[r] = mx[r] == -INFINITY ? 0.f : mx[r];
+  if (__any_sync(0xffffffff, mx[0] != m[0] || mx[1] != m[1])) {  // a running max moved: rescale
+    float alpha[2];
 #pragma unroll
-  for (int d = 0; d < 16; ++d) {
-    o[d][0] *= alpha[0];
-    o[d][1] *= alpha[0];
-    o[d][2] *= alpha[1];
-    o[d][3] *= alpha[1];
+    for (int r = 0; r < 2; ++r) {
+      alpha[r] = exp2f(m[r] - base[r]);
+      m[r] = mx[r];
+      l[r] *= alpha[r];
+    }
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      o[d][0] *= alpha[0];
+      o[d][1] *= alpha[0];
+      o[d][2] *= alpha[1];
+      o[d][3] *= alpha[1];
+    }
   }
   uint32_t pf[4][4];  // P as A fragments, one per 16-key step
 #pragma unroll
@@ -179,7 +189,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __
 #pragma unroll
     for (int d2 = 0; d2 < 8; ++d2) {
       uint32_t b[4];
-      const int row = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+      const int row = kv_row(ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3));
       const int col = d2 * 16 + ((lane >> 4) << 3);
       ldsm_x4_t(b, sv + swz(row, col));
       mma16816(o[2 * d2], pf[ks], b[0], b[1]);
@@ -222,9 +232,10 @@ __global__ void __launch_bounds__(kThreadsAttn)
                         __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t smem_attn[];
   constexpr int S = kStagesPF;
-  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_attn);  // [S][64][128]
-  __nv_bfloat16* sv = sk + S * kKT * kHD;                            // [S][64][128]
-  __nv_bfloat16* sq = sv + S * kKT * kHD;                            // [4 warps][16][128]
+  // [S][4 blocks][K 16 | V 16][128]: K view at the stage base, V view 16 rows on
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_attn);
+  __nv_bfloat16* sv = sk + 16 * kHD;
+  __nv_bfloat16* sq = sk + S * 2 * kKT * kHD;                        // [4 warps][16][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sq + 4 * 16 * kHD);
   pdl_trigger();
   const int2 wi = work[blockIdx.x];
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(kThreadsAttn)
   const uint64_t pol = policy_evict_first();
   if (threadIdx.x == 0)
     for (int t = 0; t < S && t < n_tiles; ++t)
-      issue_kv_tile(sk + t * kKT * kHD, sv + t * kKT * kHD, &full[t], kplane, vplane, pt, kv_end,
+      issue_kv_tile(sk + t * 2 * kKT * kHD, sv + t * 2 * kKT * kHD, &full[t], kplane, vplane, pt, kv_end,
                     t * kKT, kvh, g, pol);
 
   uint32_t qf[8][4];
@@ -267,11 +278,16 @@ __global__ void __launch_bounds__(kThreadsAttn)
   for (int t = 0; t < n_tiles; ++t) {
     const int buf = t % S;
     mbar_wait(&full[buf], (t / S) & 1);
-    attend_tile<true>(qf, sk + buf * kKT * kHD, sv + buf * kKT * kHD, 0, kKT, row_limit, m, l, o,
-                      g.scale_log2, t * kKT);
+    // tiles wholly below the CTA's first causal limit skip the mask math
+    if (t * kKT + kKT - 1 <= start + wi.y / g.group)
+      attend_tile<false>(qf, sk + buf * 2 * kKT * kHD, sv + buf * 2 * kKT * kHD, 0, kKT, row_limit, m, l, o,
+                         g.scale_log2, t * kKT);
+    else
+      attend_tile<true>(qf, sk + buf * 2 * kKT * kHD, sv + buf * 2 * kKT * kHD, 0, kKT, row_limit, m, l, o,
+                        g.scale_log2, t * kKT);
     __syncthreads();  // every warp is done with buf
     if (threadIdx.x == 0 && t + S < n_tiles)
-      issue_kv_tile(sk + buf * kKT * kHD, sv + buf * kKT * kHD, &full[buf], kplane, vplane, pt,
+      issue_kv_tile(sk + buf * 2 * kKT * kHD, sv + buf * 2 * kKT * kHD, &full[buf], kplane, vplane, pt,
                     kv_end, (t + S) * kKT, kvh, g, pol);
   }
   // normalize + store
@@ -299,19 +315,24 @@ __global__ void __launch_bounds__(kThreadsAttn)
 
 // Decode ("stream-K flash decoding"): the work is the flattened list of
 // 32-key tiles of every (sequence, kv head) item, ordered by sequence then
-// head. Warp w of the persistent grid owns the contiguous tile range
-// [w T / W, (w + 1) T / W) (T tiles, W warps), so every warp streams the same
-// number of KV bytes regardless of the length mix: no wave quantization, no
-// idle tails. Each warp runs its own 3-stage cp.async.bulk ring (one lane
-// issues 2 pages x K/V = 4 x 4 KB copies per tile), continuing across item
-// boundaries so the pipeline never drains. An item covered by one warp is
-// finalized in place; an item split across warps leaves (m, l, O) partials
+// head. Unit w (a warp pair) of the persistent grid owns the contiguous tile
+// range [w T / W, (w + 1) T / W) (T tiles, W units), so every unit streams
+// the same number of KV bytes regardless of the length mix: no wave
+// quantization, no idle tails. Each pair runs its own 3-stage cp.async.bulk
+// ring (one lane issues 2 pages x K/V = 4 x 4 KB copies per tile),
+// continuing across item boundaries so the pipeline never drains; warp h of
+// the pair takes keys [16 h, 16 h + 16) of every tile (two warps per SMSP
+// in the smem of one ring: the kernel is issue-latency bound, ncu 4.4
+// cycles / instruction with one warp per SMSP), and the pair merges its
+// (m, l, O) at the end of each item segment. An item covered by one unit is
+// finalized in place; an item split across units leaves (m, l, O) partials
 // that decode_combine_kernel folds with a log-sum-exp rescale.
 // The tile math is transposed (keys / head dims on the MMA's M side, the
 // G <= 8 query heads of the kv head on its N = 8 side; see the kernel).
 constexpr int kKTD = 32;      // keys per decode tile (two 16-token pages)
-constexpr int kStD = 3;       // ring stages per warp
-constexpr int kWarpsD = 4;    // warps per CTA (one CTA per SM)
+constexpr int kStD = 3;       // ring stages per pair
+constexpr int kPairsD = 4;    // warp pairs per CTA (one CTA per SM)
+constexpr int kWarpsD = 2 * kPairsD;
 constexpr int kTileD = kKTD * kHD;  // elements per K (or V) tile
 
 __device__ __forceinline__ void issue_dec_tile(__nv_bfloat16* sk, __nv_bfloat16* sv, uint64_t* bar,
@@ -324,9 +345,8 @@ __device__ __forceinline__ void issue_dec_tile(__nv_bfloat16* sk, __nv_bfloat16*
   for (int p = 0; p < 2; ++p) {
     const int key = tile * kKTD + p * 16;
     const int page = key < kv_len ? pt[key >> 4] : last_page;
-    const size_t off = (static_cast<size_t>(page) * g.n_kv_heads + kvh) * (16 * kHD);
-    bulk_load(sk + p * 16 * kHD, kplane + off, 4096, bar, policy);
-    bulk_load(sv + p * 16 * kHD, vplane + off, 4096, bar, policy);
+    const size_t off = (static_cast<size_t>(page) * g.n_kv_heads + kvh) * kKVBlock;
+    bulk_load(sk + p * kKVBlock, kplane + off, 8192, bar, policy);  // [K 16 | V 16] block
   }
 }
 
@@ -375,34 +395,40 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
                        float* __restrict__ part_ml) {
   extern __shared__ __align__(1024) uint8_t smem_attn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // per warp: [kStD][K tile][V tile] + Q staging [16][128] + kStD barriers
-  constexpr int kWarpElems = kStD * 2 * kTileD + 16 * kHD;
-  __nv_bfloat16* wbase = reinterpret_cast<__nv_bfloat16*>(smem_attn) + warp * kWarpElems;
-  __nv_bfloat16* sq = wbase + kStD * 2 * kTileD;
+  const int pair = warp >> 1, half = warp & 1;
+  // per pair: [kStD][K tile][V tile] + 2 x [8][128] fp32 staging (warp 0's
+  // doubles as the Q staging) + kStD barriers
+  constexpr int kPairElems = kStD * 2 * kTileD + 2 * 8 * kHD * 2;  // bf16 units
+  __nv_bfloat16* pbase = reinterpret_cast<__nv_bfloat16*>(smem_attn) + pair * kPairElems;
+  __nv_bfloat16* sq = pbase + kStD * 2 * kTileD;           // Q staging [8][128] bf16 (= stage_a)
+  float* stage_a = reinterpret_cast<float*>(sq);            // [8][128] fp32, warp 0
+  float* stage_b = stage_a + 8 * kHD;                       // [8][128] fp32, warp 1
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(smem_attn) +
-                                               kWarpsD * kWarpElems) + warp * kStD;
-  // W <= total warps (host), so every range holds >= 1 tile and the warps
-  // covering an item are consecutive: piece = gw - first warp of the item
+                                               kPairsD * kPairElems) + pair * kStD;
+  float* ml_b = reinterpret_cast<float*>(full + kPairsD * kStD - pair * kStD) + pair * 32;  // [8 heads][m, l]
+  const uint32_t bar_id = 1 + pair;
+  auto pair_sync = [&] { named_bar_sync(bar_id, 64); };
   pdl_trigger();
-  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsD + warp;
-  if (gw >= W) return;
+  const long long gw = static_cast<long long>(blockIdx.x) * kPairsD + pair;
+  if (gw >= W) return;  // both warps of the pair leave together
   const long long lo = total * gw / W, hi = total * (gw + 1) / W;
   const int hkv = g.n_kv_heads;
-  if (lane == 0) {
+  const bool producer = half == 0 && lane == 0;
+  if (producer) {
     for (int i = 0; i < kStD; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
-  __syncwarp();
+  pair_sync();
   pdl_wait();  // the new token's K/V and Q come from the QKV / RoPE kernels
   const uint64_t pol = policy_evict_first();
-  // producer cursor (lane 0) runs kStD tiles ahead of the consumer cursor
+  // producer cursor (one lane) runs kStD tiles ahead of the consumer cursor
   DecPos prod = dec_locate(seq_prefix, n_seq, hkv, lo);
   long long issued = lo;
-  if (lane == 0) {
+  if (producer) {
     for (; issued < hi && issued < lo + kStD; ++issued) {
       const int st = static_cast<int>(issued - lo);
       const AttnSeq ms = seqs[prod.seq];
-      issue_dec_tile(wbase + st * 2 * kTileD, wbase + st * 2 * kTileD + kTileD, &full[st], kplane,
+      issue_dec_tile(pbase + st * 2 * kTileD, pbase + st * 2 * kTileD + kTileD, &full[st], kplane,
                      vplane, pages + ms.page_off, ms.kv_len, prod.tile, prod.kvh, g, pol);
       dec_advance(prod, seq_prefix, n_seq, hkv);
     }
@@ -418,13 +444,13 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   AttnSeq meta = seqs[cur.seq];
   int seg_tile0 = cur.tile;
   const int h0 = 2 * (lane & 3);
+  const int krow = half * 16;  // this warp's 16 keys of every tile
   for (long long gt = lo; gt < hi; ++gt) {
     const int i = static_cast<int>(gt - lo), buf = i % kStD;
     if (gt == lo || cur.tile == 0) {  // new segment: this item's queries
-      __syncwarp();
       meta = seqs[cur.seq];
       seg_tile0 = cur.tile;
-      for (int c = lane; c < 8 * 16; c += 32) {
+      for (int c = half * 32 + lane; c < 8 * 16; c += 64) {
         const int r = c >> 4, chunk = c & 15;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (r < g.group)
@@ -432,7 +458,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
                                               (cur.kvh * g.group + r) * kHD + chunk * 8);
         *reinterpret_cast<uint4*>(sq + r * kHD + ((chunk ^ (r & 7)) << 3)) = v;
       }
-      __syncwarp();
+      pair_sync();
 #pragma unroll
       for (int k = 0; k < 8; k += 2) {
         uint32_t r[4];
@@ -445,74 +471,66 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
       for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     }
     mbar_wait(&full[buf], (i / kStD) & 1);
-    const __nv_bfloat16* sk = wbase + buf * 2 * kTileD;
-    const __nv_bfloat16* sv = sk + kTileD;
-    // S^T = K Q^T: 2 blocks of 16 keys x 8 k-steps
-    float s[2][4];
+    const __nv_bfloat16* sk = pbase + buf * 2 * kTileD;  // [2 blocks][K 16 | V 16][128]
+    const __nv_bfloat16* sv = sk + 16 * kHD;
+    // S^T = K Q^T over this warp's 16 keys: 8 k-steps in two chains
+    float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb) s[mb][0] = s[mb][1] = s[mb][2] = s[mb][3] = 0.f;
+    for (int k = 0; k < 8; ++k) {
+      uint32_t a[4];
+      ldsm_x4(a, sk + swz(2 * krow + (lane & 7) + (((lane >> 3) & 1) << 3), k * 16 + ((lane >> 4) << 3)));
+      mma16816((k & 1) ? s2 : s, a, qb[k][0], qb[k][1]);
+    }
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-#pragma unroll
-      for (int mb = 0; mb < 2; ++mb) {
-        uint32_t a[4];
-        ldsm_x4(a, sk + swz(mb * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), k * 16 + ((lane >> 4) << 3)));
-        mma16816(s[mb], a, qb[k][0], qb[k][1]);
-      }
+    for (int j = 0; j < 4; ++j) s[j] += s2[j];
     // mask keys past kv_len; online softmax down each head column
-    const int key0 = cur.tile * kKTD + (lane >> 2);
+    const int key0 = cur.tile * kKTD + krow + (lane >> 2);
     float mx0 = m0, mx1 = m1;
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const bool ok = key0 + mb * 16 + j * 8 < meta.kv_len;
-        s[mb][2 * j] = ok ? s[mb][2 * j] * g.scale_log2 : -INFINITY;
-        s[mb][2 * j + 1] = ok ? s[mb][2 * j + 1] * g.scale_log2 : -INFINITY;
-        mx0 = fmaxf(mx0, s[mb][2 * j]);
-        mx1 = fmaxf(mx1, s[mb][2 * j + 1]);
-      }
+    for (int j = 0; j < 2; ++j) {
+      const bool ok = key0 + j * 8 < meta.kv_len;
+      s[2 * j] = ok ? s[2 * j] * g.scale_log2 : -INFINITY;
+      s[2 * j + 1] = ok ? s[2 * j + 1] * g.scale_log2 : -INFINITY;
+      mx0 = fmaxf(mx0, s[2 * j]);
+      mx1 = fmaxf(mx1, s[2 * j + 1]);
+    }
 #pragma unroll
     for (int x = 4; x < 32; x <<= 1) {
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, x));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, x));
     }
     const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
-    const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
-    m0 = mx0, m1 = mx1;
-    l0 *= al0, l1 *= al1;
+    if (__any_sync(0xffffffff, mx0 != m0 || mx1 != m1)) {  // running max moved: rescale
+      const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
+      l0 *= al0, l1 *= al1;
 #pragma unroll
-    for (int d = 0; d < 8; ++d) o[d][0] *= al0, o[d][2] *= al0, o[d][1] *= al1, o[d][3] *= al1;
-    // P^T in C layout (keys x heads) -> B fragments (keys = k) by an 8x8 transpose
-    uint32_t pb[2][2];
-#pragma unroll
-    for (int mb = 0; mb < 2; ++mb) {
-      const float p00 = exp2f(s[mb][0] - b0), p01 = exp2f(s[mb][1] - b1);
-      const float p10 = exp2f(s[mb][2] - b0), p11 = exp2f(s[mb][3] - b1);
-      l0 += p00 + p10;
-      l1 += p01 + p11;
-      pb[mb][0] = movmatrix_trans(pack_bf16(p00, p01));
-      pb[mb][1] = movmatrix_trans(pack_bf16(p10, p11));
+      for (int d = 0; d < 8; ++d) o[d][0] *= al0, o[d][2] *= al0, o[d][1] *= al1, o[d][3] *= al1;
+      m0 = mx0, m1 = mx1;
     }
-    // O^T += V^T P^T: 8 blocks of 16 dims x 2 k-steps of 16 keys
+    // P^T in C layout (keys x heads) -> B fragments (keys = k) by an 8x8 transpose
+    const float p00 = exp2f(s[0] - b0), p01 = exp2f(s[1] - b1);
+    const float p10 = exp2f(s[2] - b0), p11 = exp2f(s[3] - b1);
+    l0 += p00 + p10;
+    l1 += p01 + p11;
+    const uint32_t pb0 = movmatrix_trans(pack_bf16(p00, p01));
+    const uint32_t pb1 = movmatrix_trans(pack_bf16(p10, p11));
+    // O^T += V^T P^T: 8 blocks of 16 dims, one k-step over this warp's keys
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-      for (int db = 0; db < 8; ++db) {
-        uint32_t a[4];
-        ldsm_x4_t(a, sv + swz(ks * 16 + (lane & 7) + ((lane >> 4) << 3), db * 16 + (((lane >> 3) & 1) << 3)));
-        mma16816(o[db], a, pb[ks][0], pb[ks][1]);
-      }
-    __syncwarp();
+    for (int db = 0; db < 8; ++db) {
+      uint32_t a[4];
+      ldsm_x4_t(a, sv + swz(2 * krow + (lane & 7) + ((lane >> 4) << 3), db * 16 + (((lane >> 3) & 1) << 3)));
+      mma16816(o[db], a, pb0, pb1);
+    }
+    pair_sync();  // both warps are done with stage buf
     // refill this stage kStD tiles ahead
-    if (lane == 0 && issued < hi) {
+    if (producer && issued < hi) {
       const AttnSeq ms = seqs[prod.seq];
-      issue_dec_tile(wbase + buf * 2 * kTileD, wbase + buf * 2 * kTileD + kTileD, &full[buf], kplane,
+      issue_dec_tile(pbase + buf * 2 * kTileD, pbase + buf * 2 * kTileD + kTileD, &full[buf], kplane,
                      vplane, pages + ms.page_off, ms.kv_len, prod.tile, prod.kvh, g, pol);
       dec_advance(prod, seq_prefix, n_seq, hkv);
       ++issued;
     }
-    // segment end: last tile of the item or of this warp's range
+    // segment end: last tile of the item or of this unit's range
     const bool item_end = cur.tile == cur.n_tiles - 1;
     if (item_end || gt == hi - 1) {
       float lt0 = l0, lt1 = l1;
@@ -521,48 +539,71 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
         lt0 += __shfl_xor_sync(0xffffffff, lt0, x);
         lt1 += __shfl_xor_sync(0xffffffff, lt1, x);
       }
-      const bool whole = seg_tile0 == 0 && item_end;
-      const float sc0 = whole ? (lt0 > 0.f ? 1.f / lt0 : 0.f) : 1.f;
-      const float sc1 = whole ? (lt1 > 0.f ? 1.f / lt1 : 0.f) : 1.f;
-      // stage [8 heads][128 dims] in the (free) Q area, then coalesced stores
-      float* so = reinterpret_cast<float*>(sq);
-      __syncwarp();
+      // merge the pair: warp 1 publishes (m, l, O), warp 0 folds
+      if (half == 1) {
 #pragma unroll
-      for (int d = 0; d < 8; ++d) {
-        const int dim = d * 16 + (lane >> 2);
-        so[h0 * kHD + dim] = o[d][0] * sc0;
-        so[(h0 + 1) * kHD + dim] = o[d][1] * sc1;
-        so[h0 * kHD + dim + 8] = o[d][2] * sc0;
-        so[(h0 + 1) * kHD + dim + 8] = o[d][3] * sc1;
-      }
-      __syncwarp();
-      if (whole) {
-        __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + cur.kvh * g.group * kHD;
-        for (int c = lane; c < g.group * 16; c += 32) {
-          const float4 u = *reinterpret_cast<const float4*>(so + c * 8);
-          const float4 v = *reinterpret_cast<const float4*>(so + c * 8 + 4);
-          uint4 w;
-          w.x = pack_bf16(u.x, u.y), w.y = pack_bf16(u.z, u.w), w.z = pack_bf16(v.x, v.y), w.w = pack_bf16(v.z, v.w);
-          *reinterpret_cast<uint4*>(dst + c * 8) = w;
+        for (int d = 0; d < 8; ++d) {
+          const int dim = d * 16 + (lane >> 2);
+          stage_b[h0 * kHD + dim] = o[d][0];
+          stage_b[(h0 + 1) * kHD + dim] = o[d][1];
+          stage_b[h0 * kHD + dim + 8] = o[d][2];
+          stage_b[(h0 + 1) * kHD + dim + 8] = o[d][3];
         }
-      } else {
-        // piece index of this warp within the item (stream-K ownership rule)
-        const long long first = ((cur.item_start + 1) * W - 1) / total;
-        const size_t slot = (static_cast<size_t>(cur.seq) * hkv + cur.kvh) * max_pieces + (gw - first);
-        float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
-        for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(so + c * 4);
         if (lane < 4) {
-          if (h0 < g.group) {
-            part_ml[(slot * g.group + h0) * 2] = m0;
-            part_ml[(slot * g.group + h0) * 2 + 1] = lt0;
+          ml_b[h0 * 2] = m0, ml_b[h0 * 2 + 1] = lt0;
+          ml_b[(h0 + 1) * 2] = m1, ml_b[(h0 + 1) * 2 + 1] = lt1;
+        }
+      }
+      pair_sync();
+      if (half == 0) {
+        const float mb0 = ml_b[h0 * 2], lb0 = ml_b[h0 * 2 + 1];
+        const float mb1 = ml_b[(h0 + 1) * 2], lb1 = ml_b[(h0 + 1) * 2 + 1];
+        const float M0 = fmaxf(m0, mb0), M1 = fmaxf(m1, mb1);
+        const float fa0 = m0 == -INFINITY ? 0.f : exp2f(m0 - M0), fb0 = mb0 == -INFINITY ? 0.f : exp2f(mb0 - M0);
+        const float fa1 = m1 == -INFINITY ? 0.f : exp2f(m1 - M1), fb1 = mb1 == -INFINITY ? 0.f : exp2f(mb1 - M1);
+        const float L0 = lt0 * fa0 + lb0 * fb0, L1 = lt1 * fa1 + lb1 * fb1;
+        const bool whole = seg_tile0 == 0 && item_end;
+        const float sa0 = fa0 * (whole ? (L0 > 0.f ? 1.f / L0 : 0.f) : 1.f);
+        const float sb0 = fb0 * (whole ? (L0 > 0.f ? 1.f / L0 : 0.f) : 1.f);
+        const float sa1 = fa1 * (whole ? (L1 > 0.f ? 1.f / L1 : 0.f) : 1.f);
+        const float sb1 = fb1 * (whole ? (L1 > 0.f ? 1.f / L1 : 0.f) : 1.f);
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          const int dim = d * 16 + (lane >> 2);
+          stage_a[h0 * kHD + dim] = o[d][0] * sa0 + stage_b[h0 * kHD + dim] * sb0;
+          stage_a[(h0 + 1) * kHD + dim] = o[d][1] * sa1 + stage_b[(h0 + 1) * kHD + dim] * sb1;
+          stage_a[h0 * kHD + dim + 8] = o[d][2] * sa0 + stage_b[h0 * kHD + dim + 8] * sb0;
+          stage_a[(h0 + 1) * kHD + dim + 8] = o[d][3] * sa1 + stage_b[(h0 + 1) * kHD + dim + 8] * sb1;
+        }
+        __syncwarp();
+        if (whole) {
+          __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + cur.kvh * g.group * kHD;
+          for (int c = lane; c < g.group * 16; c += 32) {
+            const float4 u = *reinterpret_cast<const float4*>(stage_a + c * 8);
+            const float4 v = *reinterpret_cast<const float4*>(stage_a + c * 8 + 4);
+            uint4 w;
+            w.x = pack_bf16(u.x, u.y), w.y = pack_bf16(u.z, u.w), w.z = pack_bf16(v.x, v.y), w.w = pack_bf16(v.z, v.w);
+            *reinterpret_cast<uint4*>(dst + c * 8) = w;
           }
-          if (h0 + 1 < g.group) {
-            part_ml[(slot * g.group + h0 + 1) * 2] = m1;
-            part_ml[(slot * g.group + h0 + 1) * 2 + 1] = lt1;
+        } else {
+          // piece index of this unit within the item (stream-K ownership rule)
+          const long long first = ((cur.item_start + 1) * W - 1) / total;
+          const size_t slot = (static_cast<size_t>(cur.seq) * hkv + cur.kvh) * max_pieces + (gw - first);
+          float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
+          for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(stage_a + c * 4);
+          if (lane < 4) {
+            if (h0 < g.group) {
+              part_ml[(slot * g.group + h0) * 2] = M0;
+              part_ml[(slot * g.group + h0) * 2 + 1] = L0;
+            }
+            if (h0 + 1 < g.group) {
+              part_ml[(slot * g.group + h0 + 1) * 2] = M1;
+              part_ml[(slot * g.group + h0 + 1) * 2 + 1] = L1;
+            }
           }
         }
       }
-      __syncwarp();
+      pair_sync();  // staging free again (Q of the next segment lands in stage_a)
     }
     dec_advance(cur, seq_prefix, n_seq, hkv);
   }
@@ -608,7 +649,8 @@ size_t attn_smem_bytes_pf() {
   return static_cast<size_t>(2 * kStagesPF * kKT * kHD + 4 * 16 * kHD) * 2 + 64;
 }
 size_t attn_smem_bytes_dec() {
-  return static_cast<size_t>(kWarpsD) * (kStD * 2 * kTileD + 16 * kHD) * 2 + kWarpsD * kStD * 8 + 64;
+  return static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 2 * 8 * kHD * 2) * 2 + kPairsD * kStD * 8 +
+         kPairsD * 32 * 4 + 64;
 }
 size_t attn_smem_bytes() { return std::max(attn_smem_bytes_pf(), attn_smem_bytes_dec()); }
 
@@ -634,8 +676,8 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (g.group > 8) return cudaErrorInvalidValue;
   ensure_kernels_prepared();
   const size_t smem = attn_smem_bytes_dec();
-  const long long W = std::min<long long>(static_cast<long long>(sm_count) * kWarpsD, total_tiles);
-  const int grid = static_cast<int>((W + kWarpsD - 1) / kWarpsD);
+  const long long W = std::min<long long>(static_cast<long long>(sm_count) * kPairsD, total_tiles);
+  const int grid = static_cast<int>((W + kPairsD - 1) / kPairsD);
   // pieces per item <= ceil(tiles / min range) + 1
   const long long per_min = std::max<long long>(1, total_tiles / W);
   const int max_pieces = static_cast<int>((max_seq_tiles + per_min - 1) / per_min) + 1;

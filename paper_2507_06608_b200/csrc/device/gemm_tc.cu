@@ -791,7 +791,7 @@ cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const Gemm
 static double hybrid_max_frac() {
   static const double f = [] {
     const char* e = std::getenv("NX_HYBRID_FRAC");
-    return e ? std::atof(e) : 0.85;
+    return e ? std::atof(e) : 0.0;
   }();
   return f;
 }

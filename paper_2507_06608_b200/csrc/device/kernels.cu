@@ -125,8 +125,8 @@ __device__ __forceinline__ void rope_kv_token(const __nv_bfloat16* row, __nv_bfl
         *reinterpret_cast<uint4*>(qdst + head * hd + 8 * p) = *reinterpret_cast<uint4*>(ra);
         *reinterpret_cast<uint4*>(qdst + head * hd + half + 8 * p) = *reinterpret_cast<uint4*>(rb);
       } else {
-        __nv_bfloat16* dst =
-            kplane + ((static_cast<size_t>(page) * n_kv_heads + (head - n_heads)) * page_tokens + off) * hd;
+        __nv_bfloat16* dst =  // interleaved [page][kv head][K | V][page_tokens][hd] blocks
+            kplane + ((static_cast<size_t>(page) * n_kv_heads + (head - n_heads)) * 2 * page_tokens + off) * hd;
         *reinterpret_cast<uint4*>(dst + ((p ^ sw) << 3)) = *reinterpret_cast<uint4*>(ra);
         *reinterpret_cast<uint4*>(dst + (((p + 8) ^ sw) << 3)) = *reinterpret_cast<uint4*>(rb);
       }
@@ -134,8 +134,7 @@ __device__ __forceinline__ void rope_kv_token(const __nv_bfloat16* row, __nv_bfl
       const int i = it - rot_items;
       const int kh = i >> 4, c = i & 15;
       const __nv_bfloat16* src = row + (n_heads + n_kv_heads + kh) * hd + c * 8;
-      __nv_bfloat16* dst =
-          vplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * page_tokens + off) * hd;
+      __nv_bfloat16* dst = vplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * 2 * page_tokens + off) * hd;
       *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 3)) = *reinterpret_cast<const uint4*>(src);
     }
   }

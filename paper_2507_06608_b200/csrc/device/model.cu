@@ -141,7 +141,7 @@ Model::Model(const nx_device_config& cfg, std::shared_ptr<PeerGroup> group)
   if (a_.n_heads % a_.n_kv_heads || a_.n_heads / a_.n_kv_heads > 8)
     throw std::invalid_argument("GQA group must divide heads and be <= 8");
   if (cfg.page_tokens != 16 || cfg.num_pages < 1)
-    throw std::invalid_argument("page_tokens must be 16 (4 KB pre-swizzled KV runs)");
+    throw std::invalid_argument("page_tokens must be 16 (8 KB pre-swizzled K|V blocks)");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg.device)
     throw NoDevice("no CUDA device");
@@ -551,8 +551,10 @@ void Model::forward(LaneWs& ws) {
   auto pbytes = [&](double rows) { return Td * rows * 4; };
   for (int l = 0; l < a_.n_layers; ++l) {
     const LayerW& w = layers_[l];
+    // layer l: [page][kv head][K | V][page_tokens][hd] (one contiguous 8 KB block
+    // per (page, kv head)); the V view starts one K half-block on
     __nv_bfloat16* kplane = kv_ + (2 * static_cast<size_t>(l)) * plane_elems_;
-    __nv_bfloat16* vplane = kplane + plane_elems_;
+    __nv_bfloat16* vplane = kplane + static_cast<size_t>(cfg_.page_tokens) * a_.head_dim;
     if (!fold || l == 0)
       timed(NX_K_OTHER, Td * d * 4, 0, [&] {
         ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");

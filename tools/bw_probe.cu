@@ -45,7 +45,9 @@ __global__ void stream_kernel(const __grid_constant__ CUtensorMap map, const cha
   for (int s = 0; s < stages && issued < my1; ++s, ++issued) {
     mbar_expect(&full[s], chunk);
     if (mode == 0) { long long kb = issued % 64, mb = issued / 64; tma2d(&map, &full[s], smem + s * chunk, (int)kb * 64, (int)(mb * 128) % rows); }
-    else bulk1d(smem + s * chunk, base + (issued * chunk) % (1ll << 33), chunk, &full[s]);
+    else if (mode == 1) bulk1d(smem + s * chunk, base + (issued * chunk) % (1ll << 33), chunk, &full[s]);
+    else for (int j = 0; j < chunk / 4096; ++j)  // mode 2: 4 KB pieces 32 KB apart (KV pages)
+      bulk1d(smem + s * chunk + j * 4096, base + ((issued * (chunk / 4096) + j) * 32768ll) % (1ll << 33), 4096, &full[s]);
   }
   while (done < my1) {
     mbar_wait(&full[stage], phase);
@@ -53,7 +55,9 @@ __global__ void stream_kernel(const __grid_constant__ CUtensorMap map, const cha
     if (issued < my1) {
       mbar_expect(&full[stage], chunk);
       if (mode == 0) { long long kb = issued % 64, mb = issued / 64; tma2d(&map, &full[stage], smem + stage * chunk, (int)kb * 64, (int)(mb * 128) % rows); }
-      else bulk1d(smem + stage * chunk, base + (issued * chunk) % (1ll << 33), chunk, &full[stage]);
+      else if (mode == 1) bulk1d(smem + stage * chunk, base + (issued * chunk) % (1ll << 33), chunk, &full[stage]);
+      else for (int j = 0; j < chunk / 4096; ++j)
+        bulk1d(smem + stage * chunk + j * 4096, base + ((issued * (chunk / 4096) + j) * 32768ll) % (1ll << 33), 4096, &full[stage]);
       ++issued;
     }
     if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -76,10 +80,10 @@ int main() {
   CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   struct Cfg { int mode, chunk, stages; };
-  std::vector<Cfg> cfgs = {{0, 16384, 4}, {0, 16384, 8}, {0, 16384, 12}, {1, 16384, 8}, {1, 16384, 12}, {1, 32768, 6}, {1, 65536, 3}};
+  std::vector<Cfg> cfgs = {{1, 16384, 12}, {1, 4096, 48}, {1, 4096, 12}, {2, 16384, 12}, {2, 16384, 6}, {1, 32768, 6}};
   const long long total_bytes = 2ll << 30;
   for (auto c : cfgs) {
-    for (int sms : {8, 16, 32, 64, 96, 128, 148}) {
+    for (int sms : {16, 48, 148}) {
       long long chunks = total_bytes / c.chunk;
       if (sms <= 16) chunks /= 8;
       int smem = c.stages * c.chunk + 1024;
@@ -90,7 +94,7 @@ int main() {
       float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
       double gbs = 3.0 * chunks * c.chunk / (ms * 1e-3) / 1e9;
       printf("{\"mode\": \"%s\", \"chunk\": %d, \"stages\": %d, \"sms\": %d, \"GBps\": %.0f, \"per_sm\": %.1f}\n",
-             c.mode ? "bulk1d" : "tma2d", c.chunk, c.stages, sms, gbs, gbs / sms);
+             c.mode == 2 ? "bulk4k_strided" : c.mode ? "bulk1d" : "tma2d", c.chunk, c.stages, sms, gbs, gbs / sms);
     }
   }
   return 0;
