@@ -39,11 +39,15 @@ constexpr int kRowsBlk = 256;                    // weight rows per MMA (N)
 constexpr int kKB = 64;                          // K per stage (one 128B swizzle row)
 constexpr int kWBytes = kRowsBlk * kKB * 2;      // 32 KB
 constexpr int kXBytes = 128 * kKB * 2;           // 16 KB (A tile, M = 128 rows)
-constexpr int kStage = kWBytes + kXBytes;        // 48 KB
-constexpr int kStages = 4;
+constexpr int kStagesMax = 6;
 constexpr int kThreads = 192;
 constexpr int kEpiThreads = 128;
-constexpr int kSmem = 1024 + kStages * kStage + 256;
+// Ring of `stages` stages of [W 32 KB | X box_rows x 128 B]. The MMA's A
+// operand is always a 128-row tile (16 KB); rows past the box overhang into
+// the next stage (or the slack after the ring) -- those TMEM lanes are never
+// read, so a small X box buys ring depth (weight bytes in flight per SM,
+// the bound of a partition-sized grid) instead of idle smem.
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 256;
 
 struct DecParams {
   int rows, tokens, num_kb, n_tiles;  // n_tiles = 256-row blocks
@@ -53,6 +57,8 @@ struct DecParams {
   float* out;                         // kEpiF32: [tokens][ldo]; fold: planes [piece][tokens][rows]
   int ldo;
   uint32_t x_bytes;                   // bytes of one X box (box rows x 128 B)
+  int stages;
+  uint32_t stage_bytes;               // 32 KB + x_bytes rounded up to 1 KB
 };
 
 struct DecWork {
@@ -97,9 +103,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                        DecParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  const int kStages = p.stages;
+  const uint32_t kStage = p.stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage + (kXBytes - p.x_bytes));
+  uint64_t* empty = full + kStagesMax;
+  uint64_t* tfull = empty + kStagesMax;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -252,6 +260,10 @@ cudaError_t gemm_decode(const __nv_bfloat16* w_packed, const CUtensorMap& x_map,
   p.n_tiles = (rows / 128 + 1) / 2;
   p.total = static_cast<long long>(p.n_tiles) * p.num_kb;
   p.x_bytes = static_cast<uint32_t>(box_rows) * kKB * 2;
+  p.stage_bytes = kWBytes + ((p.x_bytes + 1023u) & ~1023u);
+  p.stages = std::min<int>(kStagesMax, (kSmemBudget - 512 - (kXBytes - static_cast<int>(p.x_bytes))) /
+                                          static_cast<int>(p.stage_bytes));
+  const size_t smem = 1024 + static_cast<size_t>(p.stages) * p.stage_bytes + (kXBytes - p.x_bytes) + 512;
   p.ldo = ldo;
   int grid = std::max(1, std::min(p.n_tiles, sm_count));
   if (fold) {
@@ -297,11 +309,11 @@ cudaError_t gemm_decode(const __nv_bfloat16* w_packed, const CUtensorMap& x_map,
   }
   ensure_kernels_prepared();
   ++g_kernel_launches;
-  return launch_pdl(gemm_decode_kernel, dim3(grid), dim3(kThreads), kSmem, stream, w_packed, x_map, p);
+  return launch_pdl(gemm_decode_kernel, dim3(grid), dim3(kThreads), smem, stream, w_packed, x_map, p);
 }
 
 void prepare_gemm_decode_kernel() {
-  cudaFuncSetAttribute(gemm_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  cudaFuncSetAttribute(gemm_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
 }
 
 }  // namespace nxd

@@ -646,7 +646,7 @@ void Model::forward(LaneWs& ws) {
     const int sbn = gemm_pick_bn(n);
     timed(gk, static_cast<double>(vocab_l_) * d * 2 + nd * d * 2 + nd * vocab_l_ * 4,
           2.0 * nd * vocab_l_ * d, [&] {
-            ck(fold && n <= 128
+            ck(tp_ == 1 && n <= 128
                    ? gemm_decode(lm_head_, ws.map_hs[bn_index(sbn)], sbn, vocab_l_, n, d, ws.logits, vocab_l_,
                                  ws.ws, ws.ws_bytes, sm, s, nullptr)
                    : gemm(lm_head_, ws.map_hs[bn_index(sbn)], sbn, vocab_l_, n, d, kEpiF32, ws.logits,
