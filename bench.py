@@ -378,9 +378,20 @@ def main():
             ach, peak, unit = c["TFLOPs"], pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), "TFLOP/s"
         else:
             ach, peak, unit = c["GBps"], pk["hbm_gbs"], "GB/s"
+        alg_bytes = ks.bytes[i] / ks.launches[i]
+        traffic, traffic_src = None, None
+        try:  # DRAM bytes / algorithmic bytes of this kernel class from one ncu --set full capture
+            with open(os.path.join(REPO, "profiles", "dram_traffic.json")) as f:
+                t = json.load(f).get(dom)
+            if t:
+                traffic, traffic_src = t["dram_over_algorithmic"] * alg_bytes, t["source"]
+        except (OSError, ValueError):
+            pass
         roof = {"bound": "tensor" if tensor else "hbm", "kernel_class": dom, "achieved": ach, "peak": peak,
                 "peak_source": pk_kind + (" sustained" if tensor else ""), "unit": unit,
-                "frac": ach / peak if peak else None, "traffic": None,
+                "frac": ach / peak if peak else None,
+                "traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": alg_bytes,
                 "algorithmic_per_launch": (ks.flops[i] if tensor else ks.bytes[i]) / ks.launches[i],
                 "share_of_sampled_device_time": ks.ms[i] / ks.batch_ms_sampled if ks.batch_ms_sampled else None}
     if rank != 0:

@@ -77,6 +77,7 @@ struct GemmParams {
   int dbg;         // experiments only (NX_GEMM_DBG): 1 skip X loads, 2 skip MMAs
   int fold;        // 1: every work item writes fp32 planes, no fix-up (see GemmFold)
   int sk_tile0;    // stream-K covers tiles [sk_tile0, tiles); earlier tiles run data-parallel
+  int bn_rt;       // token tile width (MMA N) of this launch, <= the template BN
 };
 
 int gemm_pick_bn(int tokens);

@@ -222,8 +222,8 @@ __device__ __forceinline__ void streamk_arrive(const GemmParams& p, const Work& 
   named_bar_sync(1, kEpiThreads);
   if (!*s_flag) return;
   __threadfence();
-  const int tok_base = w.n_blk * BN;
-  const int n_tok = min(BN, p.tokens - tok_base);
+  const int tok_base = w.n_blk * p.bn_rt;
+  const int n_tok = min(p.bn_rt, p.tokens - tok_base);
   const float4* base = reinterpret_cast<const float4*>(
       p.ws + static_cast<size_t>(tile) * p.max_pieces * MT * BN * kBM);
   constexpr int kSlot4 = BN * kBM / 4;  // float4 per (piece, sub-tile) slot
@@ -359,8 +359,8 @@ __device__ void streamk_reduce_slice(const GemmParams& p, int m_blk, int n_blk, 
   const int piece = static_cast<int>(blockIdx.x) - first;
   int* arrive = p.tile_count + tile;
   int* depart = p.tile_count + kGemmMaxCounterTiles + tile;
-  const int tok_base = n_blk * BN;
-  const int n_tok = min(BN, p.tokens - tok_base);
+  const int tok_base = n_blk * p.bn_rt;
+  const int n_tok = min(p.bn_rt, p.tokens - tok_base);
   const int valid = min(MT, p.n_tiles128 - m_blk * MT);
   const int R = valid * n_tok;
   const int r0 = R * piece / pieces, r1 = R * (piece + 1) / pieces;
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(&full[stage], valid * kABytes + stage_bytes_x);
             load_w(w, kb, valid, sa, &full[stage]);
           }
-          if (!(p.dbg & 1)) tma_load_2d(&tx, &full[stage], sa + MT * kABytes, kb * kBK, w.n_blk * BN);
+          if (!(p.dbg & 1)) tma_load_2d(&tx, &full[stage], sa + MT * kABytes, kb * kBK, w.n_blk * p.bn_rt);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+    const uint32_t idesc = umma_idesc_bf16(kBM, p.bn_rt);  // runtime N <= BN (prefill wave fit)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
@@ -583,11 +583,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int valid = min(MT, p.n_tiles128 - w.m_blk * MT);
       for (int sub = 0; sub < valid; ++sub)
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = 0; c0 < p.bn_rt; c0 += 32) {
         const int m128 = w.m_blk * MT + sub;
         const int f0 = m128 * kBM;
-        const int tok0 = w.n_blk * BN + c0;
-        if (tok0 >= p.tokens) break;
+        const int tok0 = w.n_blk * p.bn_rt + c0;
+        const int tlim = min(p.tokens, (w.n_blk + 1) * p.bn_rt);  // this tile's token rows
+        if (tok0 >= tlim) break;
         // residual rows of this 32-token chunk: issued before the TMEM load
         // so their global latency overlaps the accumulator staging
         const bool has_res = !w.partial && !p.fold && (p.mode == kEpiResidual || p.mode == kEpiBiasResidual);
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int pass = 0; pass < 4; ++pass) {
             const int t = tok0 + pass * 8 + (et >> 4);
-            res[pass] = t < p.tokens ? *reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(t) * p.ldr +
+            res[pass] = t < tlim ? *reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(t) * p.ldr +
                                                                       f0 + g * 8)
                                      : make_uint4(0, 0, 0, 0);
           }
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int pass = 0; pass < 8; ++pass) {
             const int j = pass * 4 + (et >> 5);
             const int t = tok0 + j;
-            if (t < p.tokens) {
+            if (t < tlim) {
               const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
               float* dst =
                   p.fold      ? p.ws + (static_cast<size_t>(w.piece) * p.tokens + t) * p.rows + f0 + g * 4
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int pass = 0; pass < 2; ++pass) {
             const int j = pass * 16 + (et >> 3);
             const int t = tok0 + j;
-            if (t < p.tokens) {
+            if (t < tlim) {
               __align__(16) __nv_bfloat16 o[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int pass = 0; pass < 8; ++pass) {
             const int j = pass * 4 + (et >> 5);
             const int t = tok0 + j;
-            if (t < p.tokens) {
+            if (t < tlim) {
               const float4 v = *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
               float* dst = static_cast<float*>(p.out) + static_cast<size_t>(t) * p.ldo + f0 + g * 4;
               *reinterpret_cast<float4*>(dst) = v;
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int pass = 0; pass < 4; ++pass) {
             const int j = pass * 8 + (et >> 4);
             const int t = tok0 + j;
-            if (t < p.tokens) {
+            if (t < tlim) {
               float v[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) v[i] = s_epi[j * kBM + g * 8 + i];
@@ -786,6 +787,15 @@ cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const Gemm
 
 }  // namespace
 
+// NX_BN_FIT=0 keeps N = 256 for every prefill tile.
+static bool bn_fit_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("NX_BN_FIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Prefill hybrid stream-K applies when the last wave is at most this full
 // (NX_HYBRID_FRAC; 0 disables).
 static double hybrid_max_frac() {
@@ -839,7 +849,26 @@ cudaError_t gemm(const __nv_bfloat16* w_map, const CUtensorMap& x_map_for_bn, in
   const int mt = (bn <= 64 && sm_count <= 24) ? 2 : 1;
   p.n_tiles128 = rows / kBM;
   p.n_mblk = (p.n_tiles128 + mt - 1) / mt;
-  p.n_nblk = (tokens + bn - 1) / bn;
+  // Prefill (BN = 256): the token tile width N is a runtime choice in
+  // [192, 256] (multiples of 16) that fits the tile count to whole waves of
+  // the partition -- e.g. T = 1450 on 112 SMs: o / down have 32 x 6 = 192
+  // tiles (1.7 waves) at N = 256, 32 x 7 = 224 (2.0 waves) at N = 208. MMAs
+  // with N >= ~200 stay near the tensor floor (N <= 128 costs ~100 cycles
+  // regardless, tools/mma_probe.cu), so narrower tiles are not an option.
+  p.bn_rt = bn;
+  if (bn == 256 && force_splits == 0 && !fold && bn_fit_enabled()) {
+    long long best = -1;
+    for (int n = 256; n >= 192; n -= 16) {
+      const long long tiles_n = static_cast<long long>(p.n_mblk) * ((tokens + n - 1) / n);
+      const long long waves = (tiles_n + sm_count - 1) / sm_count;
+      // tile time ~ half fixed (weight / activation staging, epilogue per tile),
+      // half MMA (cycles ~ max(N, 208) per K16 step, tools/mma_probe.cu); measured:
+      // gate_up at 12 vs 14 waves of N = 256 vs 208 was 10% faster at 256
+      const long long cost = waves * (std::max(n, 208) + 256);
+      if (best < 0 || cost < best) best = cost, p.bn_rt = n;
+    }
+  }
+  p.n_nblk = (tokens + p.bn_rt - 1) / p.bn_rt;
   p.num_kb = K / kBK;
   p.mode = mode;
   p.out = out;

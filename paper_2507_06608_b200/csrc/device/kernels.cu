@@ -29,20 +29,25 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat1
   for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) dst[i] = src[i];
 }
 
-// One CTA (256 threads) per row; fp32 sum of squares, bf16 in/out.
-__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows,
-                               int hidden, const __nv_bfloat16* __restrict__ w, float eps,
-                               __nv_bfloat16* __restrict__ out) {
+// One CTA per row, one 16 B chunk per thread (blockDim = hidden / 8, <= 1024;
+// up to 2 chunks per thread beyond): the row is read once into registers.
+__global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      const int32_t* __restrict__ rows, int hidden,
+                                                      const __nv_bfloat16* __restrict__ w, float eps,
+                                                      __nv_bfloat16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
   const int src_row = rows ? rows[r] : r;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(src_row) * hidden);
   const int nvec = hidden / 8;
+  uint4 v[2];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-    const uint4 v = xr[i];
-    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int i = threadIdx.x + c * blockDim.x;
+    v[c] = i < nvec ? xr[i] : make_uint4(0, 0, 0, 0);
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v[c]);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float f = __bfloat162float(b[k]);
@@ -54,19 +59,17 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  const float inv = rsqrtf(red[0] / hidden + eps);
+  float tot = 0.f;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += red[i];
+  const float inv = rsqrtf(tot / hidden + eps);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(r) * hidden);
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-    const uint4 v = xr[i], ww = wr[i];
-    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int i = threadIdx.x + c * blockDim.x;
+    if (i >= nvec) break;
+    const uint4 ww = wr[i];
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v[c]);
     const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(&ww);
     __align__(16) __nv_bfloat16 o[8];
 #pragma unroll
@@ -436,7 +439,10 @@ cudaError_t rmsnorm(const __nv_bfloat16* x, const int32_t* rows, int n, int hidd
                     const __nv_bfloat16* w, float eps, __nv_bfloat16* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ++g_kernel_launches;
-  return launch_pdl(rmsnorm_kernel, dim3(n), dim3(256), 0, s, x, rows, hidden, w, eps, out);
+  if (hidden % 8 || hidden > 2 * 8 * 512) return cudaErrorInvalidValue;
+  const int nvec = hidden / 8;  // 16 B chunks: one per thread, two beyond 512 threads
+  const int threads = ((nvec > 512 ? (nvec + 1) / 2 : nvec) + 31) / 32 * 32;
+  return launch_pdl(rmsnorm_kernel, dim3(n), dim3(threads), 0, s, x, rows, hidden, w, eps, out);
 }
 
 cudaError_t rope_table(const int32_t* pos, int n_tokens, const float* inv_freq, int head_dim,

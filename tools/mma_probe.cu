@@ -75,7 +75,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&d, 1024 * 8);
   unsigned long long h[1024];
   const int rounds = 256;
-  for (int n : {32, 64, 128, 256})
+  for (int n : {32, 64, 128, 160, 192, 208, 224, 240, 256})
     for (int chains : {1, 2, 4})
       for (int il : {0, 1}) {
         if (chains * n > 512 || (chains == 1 && il)) continue;

@@ -7,11 +7,15 @@ from paper_2507_06608_b200 import device as D
 B = int(os.environ.get("B", "64")); CTX = int(os.environ.get("CTX", "600"))
 DPCT = int(os.environ.get("DPCT", "100")); PPCT = int(os.environ.get("PPCT", "100"))
 REPS = int(os.environ.get("REPS", "3")); MODE = os.environ.get("MODE", "decode")
-dev = D.Device(D.arch_preset("llama3-8b"), num_pages=B * (CTX // 16 + 2) + 600, max_decode_batch=max(64, B))
+dev = D.Device(D.arch_preset("llama3-8b"), num_pages=B * (CTX // 16 + 2) + 1200, max_decode_batch=max(64, B))
 rng = np.random.default_rng(0)
 pp = CTX // 16 + 2
 Dm = [dict(tokens=[int(rng.integers(0, 1000))], start=CTX - 1, pages=list(range(i * pp, (i + 1) * pp))) for i in range(B)]
-P = [dict(tokens=rng.integers(0, 1000, 512).tolist(), start=0, pages=list(range(B * pp + 40 * i, B * pp + 40 * i + 33))) for i in range(4)]
+PLENS = [int(x) for x in os.environ.get("PLENS", "512,512,512,512").split(",")]
+P, pg0 = [], B * pp
+for n in PLENS:
+    P.append(dict(tokens=rng.integers(0, 1000, n).tolist(), start=0, pages=list(range(pg0, pg0 + n // 16 + 1))))
+    pg0 += n // 16 + 1
 import time
 for r in range(REPS):
     if MODE in ("decode", "both"):
