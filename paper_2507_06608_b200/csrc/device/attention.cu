@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "device.cuh"
 #include "ptx.cuh"
@@ -47,13 +49,26 @@ __device__ __forceinline__ int swz(int row, int col) {
   return row * kHD + ((((col >> 3) ^ (row & 7)) << 3) | (col & 7));
 }
 
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+// Shared-window addresses (uint32): the generic-pointer forms below cost a
+// cvta per ldmatrix, which was ~25% of the decode kernel's instructions (ncu).
+__device__ __forceinline__ void ldsm_x4_s(uint32_t (&r)[4], uint32_t a) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(p)));
+               : "r"(a));
 }
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+__device__ __forceinline__ void ldsm_x4_t_s(uint32_t (&r)[4], uint32_t a) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+// 2^x on the SFU (ftz; 2^-inf = 0): exp2f adds range fix-ups around MUFU.EX2.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
@@ -100,8 +115,8 @@ __device__ __forceinline__ void issue_kv_tile(__nv_bfloat16* sk, __nv_bfloat16* 
 // One warp: 16 query rows against a 64-key tile already staged in smem.
 // Updates the running max / sum and the 16 x 128 output accumulator.
 template <bool kMask>
-__device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __nv_bfloat16* sk,
-                                            const __nv_bfloat16* sv, int key_lo, int key_hi,
+__device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], uint32_t sk, uint32_t sv,
+                                            int key_lo, int key_hi,
                                             const int (&row_limit)[2], float (&m)[2],
                                             float (&l)[2], float (&o)[16][4], float scale_log2,
                                             int key0) {
@@ -121,7 +136,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __
       uint32_t b[4];
       const int row = kv_row(kb + (lane & 7) + ((lane >> 4) << 3));
       const int col = k * 16 + (((lane >> 3) & 1) << 3);
-      ldsm_x4(b, sk + swz(row, col));
+      ldsm_x4_s(b, sk + 2 * swz(row, col));
       mma16816(s[2 * n2], qf[k], b[0], b[1]);
       mma16816(s[2 * n2 + 1], qf[k], b[2], b[3]);
     }
@@ -152,7 +167,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __
     float alpha[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      alpha[r] = exp2f(m[r] - base[r]);
+      alpha[r] = ex2(m[r] - base[r]);
       m[r] = mx[r];
       l[r] *= alpha[r];
     }
@@ -170,7 +185,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __
     float p[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      p[i] = exp2f(s[n][i] - base[i >> 1]);
+      p[i] = ex2(s[n][i] - base[i >> 1]);
       l[i >> 1] += p[i];
     }
     const int ks = n >> 1;
@@ -191,7 +206,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], const __
       uint32_t b[4];
       const int row = kv_row(ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3));
       const int col = d2 * 16 + ((lane >> 4) << 3);
-      ldsm_x4_t(b, sv + swz(row, col));
+      ldsm_x4_t_s(b, sv + 2 * swz(row, col));
       mma16816(o[2 * d2], pf[ks], b[0], b[1]);
       mma16816(o[2 * d2 + 1], pf[ks], b[2], b[3]);
     }
@@ -235,6 +250,7 @@ __global__ void __launch_bounds__(kThreadsAttn)
   // [S][4 blocks][K 16 | V 16][128]: K view at the stage base, V view 16 rows on
   __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem_attn);
   __nv_bfloat16* sv = sk + 16 * kHD;
+  const uint32_t sk_s = smem_u32(sk), sv_s = smem_u32(sv);
   __nv_bfloat16* sq = sk + S * 2 * kKT * kHD;                        // [4 warps][16][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sq + 4 * 16 * kHD);
   pdl_trigger();
@@ -280,11 +296,11 @@ __global__ void __launch_bounds__(kThreadsAttn)
     mbar_wait(&full[buf], (t / S) & 1);
     // tiles wholly below the CTA's first causal limit skip the mask math
     if (t * kKT + kKT - 1 <= start + wi.y / g.group)
-      attend_tile<false>(qf, sk + buf * 2 * kKT * kHD, sv + buf * 2 * kKT * kHD, 0, kKT, row_limit, m, l, o,
-                         g.scale_log2, t * kKT);
+      attend_tile<false>(qf, sk_s + buf * 2 * kKT * kHD * 2, sv_s + buf * 2 * kKT * kHD * 2, 0, kKT, row_limit, m,
+                         l, o, g.scale_log2, t * kKT);
     else
-      attend_tile<true>(qf, sk + buf * 2 * kKT * kHD, sv + buf * 2 * kKT * kHD, 0, kKT, row_limit, m, l, o,
-                        g.scale_log2, t * kKT);
+      attend_tile<true>(qf, sk_s + buf * 2 * kKT * kHD * 2, sv_s + buf * 2 * kKT * kHD * 2, 0, kKT, row_limit, m, l,
+                        o, g.scale_log2, t * kKT);
     __syncthreads();  // every warp is done with buf
     if (threadIdx.x == 0 && t + S < n_tiles)
       issue_kv_tile(sk + buf * 2 * kKT * kHD, sv + buf * 2 * kKT * kHD, &full[buf], kplane, vplane, pt,
@@ -400,6 +416,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   // doubles as the Q staging) + kStD barriers
   constexpr int kPairElems = kStD * 2 * kTileD + 2 * 8 * kHD * 2;  // bf16 units
   __nv_bfloat16* pbase = reinterpret_cast<__nv_bfloat16*>(smem_attn) + pair * kPairElems;
+  const uint32_t pbase_s = smem_u32(pbase);
   __nv_bfloat16* sq = pbase + kStD * 2 * kTileD;           // Q staging [8][128] bf16 (= stage_a)
   float* stage_a = reinterpret_cast<float*>(sq);            // [8][128] fp32, warp 0
   float* stage_b = stage_a + 8 * kHD;                       // [8][128] fp32, warp 1
@@ -471,14 +488,15 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
       for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     }
     mbar_wait(&full[buf], (i / kStD) & 1);
-    const __nv_bfloat16* sk = pbase + buf * 2 * kTileD;  // [2 blocks][K 16 | V 16][128]
-    const __nv_bfloat16* sv = sk + 16 * kHD;
+    // [2 blocks][K 16 | V 16][128]; shared-window byte addresses
+    const uint32_t sk = pbase_s + static_cast<uint32_t>(buf * 2 * kTileD * 2);
+    const uint32_t sv = sk + 16 * kHD * 2;
     // S^T = K Q^T over this warp's 16 keys: 8 k-steps in two chains
     float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       uint32_t a[4];
-      ldsm_x4(a, sk + swz(2 * krow + (lane & 7) + (((lane >> 3) & 1) << 3), k * 16 + ((lane >> 4) << 3)));
+      ldsm_x4_s(a, sk + 2 * swz(2 * krow + (lane & 7) + (((lane >> 3) & 1) << 3), k * 16 + ((lane >> 4) << 3)));
       mma16816((k & 1) ? s2 : s, a, qb[k][0], qb[k][1]);
     }
 #pragma unroll
@@ -501,15 +519,15 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
     }
     const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
     if (__any_sync(0xffffffff, mx0 != m0 || mx1 != m1)) {  // running max moved: rescale
-      const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
+      const float al0 = ex2(m0 - b0), al1 = ex2(m1 - b1);
       l0 *= al0, l1 *= al1;
 #pragma unroll
       for (int d = 0; d < 8; ++d) o[d][0] *= al0, o[d][2] *= al0, o[d][1] *= al1, o[d][3] *= al1;
       m0 = mx0, m1 = mx1;
     }
     // P^T in C layout (keys x heads) -> B fragments (keys = k) by an 8x8 transpose
-    const float p00 = exp2f(s[0] - b0), p01 = exp2f(s[1] - b1);
-    const float p10 = exp2f(s[2] - b0), p11 = exp2f(s[3] - b1);
+    const float p00 = ex2(s[0] - b0), p01 = ex2(s[1] - b1);
+    const float p10 = ex2(s[2] - b0), p11 = ex2(s[3] - b1);
     l0 += p00 + p10;
     l1 += p01 + p11;
     const uint32_t pb0 = movmatrix_trans(pack_bf16(p00, p01));
@@ -518,7 +536,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 #pragma unroll
     for (int db = 0; db < 8; ++db) {
       uint32_t a[4];
-      ldsm_x4_t(a, sv + swz(2 * krow + (lane & 7) + ((lane >> 4) << 3), db * 16 + (((lane >> 3) & 1) << 3)));
+      ldsm_x4_t_s(a, sv + 2 * swz(2 * krow + (lane & 7) + ((lane >> 4) << 3), db * 16 + (((lane >> 3) & 1) << 3)));
       mma16816(o[db], a, pb0, pb1);
     }
     pair_sync();  // both warps are done with stage buf
@@ -559,8 +577,8 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
         const float mb0 = ml_b[h0 * 2], lb0 = ml_b[h0 * 2 + 1];
         const float mb1 = ml_b[(h0 + 1) * 2], lb1 = ml_b[(h0 + 1) * 2 + 1];
         const float M0 = fmaxf(m0, mb0), M1 = fmaxf(m1, mb1);
-        const float fa0 = m0 == -INFINITY ? 0.f : exp2f(m0 - M0), fb0 = mb0 == -INFINITY ? 0.f : exp2f(mb0 - M0);
-        const float fa1 = m1 == -INFINITY ? 0.f : exp2f(m1 - M1), fb1 = mb1 == -INFINITY ? 0.f : exp2f(mb1 - M1);
+        const float fa0 = m0 == -INFINITY ? 0.f : ex2(m0 - M0), fb0 = mb0 == -INFINITY ? 0.f : ex2(mb0 - M0);
+        const float fa1 = m1 == -INFINITY ? 0.f : ex2(m1 - M1), fb1 = mb1 == -INFINITY ? 0.f : ex2(mb1 - M1);
         const float L0 = lt0 * fa0 + lb0 * fb0, L1 = lt1 * fa1 + lb1 * fb1;
         const bool whole = seg_tile0 == 0 && item_end;
         const float sa0 = fa0 * (whole ? (L0 > 0.f ? 1.f / L0 : 0.f) : 1.f);
@@ -634,7 +652,7 @@ __global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ se
   for (int q = 0; q < pieces; ++q) {
     const size_t slot = slot0 + static_cast<size_t>(q) * g.group;
     const float ms = part_ml[slot * 2];
-    const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+    const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
     L += part_ml[slot * 2 + 1] * w;
     acc += part_o[slot * kHD + d] * w;
   }
@@ -642,6 +660,252 @@ __global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ se
       __float2bfloat16(L > 0.f ? acc / L : 0.f);
 }
 
+
+// Decode, page-major variant: a CTA of Hkv warps (warp w = kv head w) streams
+// whole pages of one sequence -- [page][kv head][K | V] makes a page of all
+// kv heads one contiguous Hkv x 8 KB block, so every stage is a single
+// 64 KB cp.async.bulk (bulk copies pay a per-copy cost: 4-8 KB copies cap a
+// warp-pair ring at ~55-60 GB/s/SM, tools/bw_probe.cu). Unit u of the
+// persistent grid owns the 32-key tiles [u T / W, (u + 1) T / W) of the
+// sequence-major tile list (T = seq_prefix[n_seq]); a tile is two page
+// stages. Per warp and stage the math is the transposed 16-key step of the
+// pair kernel (S^T = K Q^T, O^T += V^T P^T). A sequence covered by one unit
+// is finalized in place; otherwise units write (m, l, O) partials per kv head
+// and decode_combine_pages_kernel folds them.
+constexpr int kStPg = 3;  // page stages per CTA ring
+
+__global__ void __launch_bounds__(8 * 32, 1)
+    decode_attn_pages_kernel(AttnGeom g, const __nv_bfloat16* __restrict__ qkv,
+                             const __nv_bfloat16* __restrict__ kvbase, const AttnSeq* __restrict__ seqs,
+                             const int* __restrict__ seq_prefix, int n_seq, long long total, long long W,
+                             const int32_t* __restrict__ pages, int max_pieces, __nv_bfloat16* __restrict__ out,
+                             float* __restrict__ part_o, float* __restrict__ part_ml) {
+  extern __shared__ __align__(1024) uint8_t smem_attn[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hkv = g.n_kv_heads;
+  const int stage_elems = hkv * kKVBlock;
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(smem_attn);
+  const uint32_t ring_s = smem_u32(ring);
+  float* wstage = reinterpret_cast<float*>(ring + kStPg * stage_elems) + warp * 8 * kHD;  // [8][128] fp32
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(wstage);                           // Q staging [8][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(ring + kStPg * stage_elems) + hkv * 8 * kHD);
+  pdl_trigger();
+  const long long u = blockIdx.x;
+  if (u >= W) return;
+  const long long lo = total * u / W, hi = total * (u + 1) / W;  // 32-key tiles
+  const bool producer = threadIdx.x == 0;
+  if (producer) {
+    for (int i = 0; i < kStPg; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();  // the new token's K/V and Q come from the QKV / RoPE kernels
+  const uint64_t pol = policy_evict_first();
+  const uint32_t stage_bytes = static_cast<uint32_t>(stage_elems) * 2;
+  // tile gt -> (sequence, tile within it): the unit's first tile by binary search
+  auto locate = [&](long long gt, int& seq) {
+    int a = 0, b = n_seq - 1;
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (seq_prefix[mid] <= gt) a = mid;
+      else b = mid - 1;
+    }
+    seq = a;
+  };
+  // producer: stage j of the range = page (j & 1) of tile lo + j / 2
+  int pseq = 0;
+  locate(lo, pseq);
+  const long long n_stages = 2 * (hi - lo);
+  long long issued = 0;
+  auto issue = [&](long long j) {
+    const long long gt = lo + j / 2;
+    while (pseq + 1 < n_seq && seq_prefix[pseq + 1] <= gt) ++pseq;
+    const AttnSeq ms = seqs[pseq];
+    const int key = static_cast<int>(gt - seq_prefix[pseq]) * kKTD + static_cast<int>(j & 1) * 16;
+    const int32_t* pt = pages + ms.page_off;
+    // keys past kv_len re-load the last valid page: masked, finite data
+    const int page = key < ms.kv_len ? pt[key >> 4] : pt[(ms.kv_len - 1) >> 4];
+    const int st = static_cast<int>(j % kStPg);
+    mbar_expect_tx(&full[st], stage_bytes);
+    bulk_load(ring + st * stage_elems, kvbase + static_cast<size_t>(page) * stage_elems, stage_bytes, &full[st],
+              pol);
+  };
+  if (producer)
+    for (; issued < n_stages && issued < kStPg; ++issued) issue(issued);
+
+  const bool live = warp < hkv;
+  uint32_t qb[8][2];
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  float o[8][4];
+  const int h0 = 2 * (lane & 3);
+  int seq = 0;
+  locate(lo, seq);
+  AttnSeq meta = seqs[seq];
+  long long seg_tile0 = lo;
+  for (long long j = 0; j < n_stages; ++j) {
+    const long long gt = lo + j / 2;
+    const int half = static_cast<int>(j & 1);
+    if (j == 0 || (half == 0 && gt == seq_prefix[seq + 1])) {  // new segment (sequence)
+      if (j > 0) ++seq;
+      meta = seqs[seq];
+      seg_tile0 = gt;
+      if (live) {
+        for (int c = lane; c < 8 * 16; c += 32) {
+          const int r = c >> 4, chunk = c & 15;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (r < g.group)
+            v = *reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(meta.q_start) * g.qkv_stride +
+                                                (warp * g.group + r) * kHD + chunk * 8);
+          *reinterpret_cast<uint4*>(sq + r * kHD + ((chunk ^ (r & 7)) << 3)) = v;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          uint32_t r[4];
+          ldsm_x4(r, sq + swz(lane & 7, k * 16 + ((lane >> 3) << 3)));
+          qb[k][0] = r[0], qb[k][1] = r[1], qb[k + 1][0] = r[2], qb[k + 1][1] = r[3];
+        }
+        m0 = m1 = -INFINITY;
+        l0 = l1 = 0.f;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
+      }
+    }
+    const int st = static_cast<int>(j % kStPg);
+    mbar_wait(&full[st], static_cast<uint32_t>((j / kStPg) & 1));
+    const int key0 = static_cast<int>(gt - seq_prefix[seq]) * kKTD + half * 16;
+    if (live && key0 < meta.kv_len) {
+      const uint32_t sk = ring_s + static_cast<uint32_t>((st * stage_elems + warp * kKVBlock) * 2);  // [K 16 | V 16]
+      const uint32_t sv = sk + 16 * kHD * 2;
+      float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t a[4];
+        ldsm_x4_s(a, sk + 2 * swz((lane & 7) + (((lane >> 3) & 1) << 3), k * 16 + ((lane >> 4) << 3)));
+        mma16816((k & 1) ? s2 : s, a, qb[k][0], qb[k][1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[i] += s2[i];
+      const int kq = key0 + (lane >> 2);
+      float mx0 = m0, mx1 = m1;
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const bool ok = kq + jj * 8 < meta.kv_len;
+        s[2 * jj] = ok ? s[2 * jj] * g.scale_log2 : -INFINITY;
+        s[2 * jj + 1] = ok ? s[2 * jj + 1] * g.scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, s[2 * jj]);
+        mx1 = fmaxf(mx1, s[2 * jj + 1]);
+      }
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, x));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, x));
+      }
+      const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
+      if (__any_sync(0xffffffff, mx0 != m0 || mx1 != m1)) {
+        const float al0 = ex2(m0 - b0), al1 = ex2(m1 - b1);
+        l0 *= al0, l1 *= al1;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) o[d][0] *= al0, o[d][2] *= al0, o[d][1] *= al1, o[d][3] *= al1;
+        m0 = mx0, m1 = mx1;
+      }
+      const float p00 = ex2(s[0] - b0), p01 = ex2(s[1] - b1);
+      const float p10 = ex2(s[2] - b0), p11 = ex2(s[3] - b1);
+      l0 += p00 + p10;
+      l1 += p01 + p11;
+      const uint32_t pb0 = movmatrix_trans(pack_bf16(p00, p01));
+      const uint32_t pb1 = movmatrix_trans(pack_bf16(p10, p11));
+#pragma unroll
+      for (int db = 0; db < 8; ++db) {
+        uint32_t a[4];
+        ldsm_x4_t_s(a, sv + 2 * swz((lane & 7) + ((lane >> 4) << 3), db * 16 + (((lane >> 3) & 1) << 3)));
+        mma16816(o[db], a, pb0, pb1);
+      }
+    }
+    __syncthreads();  // every warp is done with stage st
+    if (producer && issued < n_stages) issue(issued++);
+    // segment end: last stage of the sequence or of the unit's range
+    const bool seq_end = half == 1 && gt + 1 == seq_prefix[seq + 1];
+    if (live && (seq_end || j == n_stages - 1)) {
+      float lt0 = l0, lt1 = l1;
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1) {
+        lt0 += __shfl_xor_sync(0xffffffff, lt0, x);
+        lt1 += __shfl_xor_sync(0xffffffff, lt1, x);
+      }
+      const bool whole = seg_tile0 == seq_prefix[seq] && seq_end;
+      const float sc0 = whole ? (lt0 > 0.f ? 1.f / lt0 : 0.f) : 1.f;
+      const float sc1 = whole ? (lt1 > 0.f ? 1.f / lt1 : 0.f) : 1.f;
+      __syncwarp();
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        const int dim = d * 16 + (lane >> 2);
+        wstage[h0 * kHD + dim] = o[d][0] * sc0;
+        wstage[(h0 + 1) * kHD + dim] = o[d][1] * sc1;
+        wstage[h0 * kHD + dim + 8] = o[d][2] * sc0;
+        wstage[(h0 + 1) * kHD + dim + 8] = o[d][3] * sc1;
+      }
+      __syncwarp();
+      if (whole) {
+        __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + warp * g.group * kHD;
+        for (int c = lane; c < g.group * 16; c += 32) {
+          const float4 a = *reinterpret_cast<const float4*>(wstage + c * 8);
+          const float4 b = *reinterpret_cast<const float4*>(wstage + c * 8 + 4);
+          uint4 w;
+          w.x = pack_bf16(a.x, a.y), w.y = pack_bf16(a.z, a.w), w.z = pack_bf16(b.x, b.y), w.w = pack_bf16(b.z, b.w);
+          *reinterpret_cast<uint4*>(dst + c * 8) = w;
+        }
+      } else {
+        const long long first = ((static_cast<long long>(seq_prefix[seq]) + 1) * W - 1) / total;
+        const size_t slot = (static_cast<size_t>(seq) * hkv + warp) * max_pieces + static_cast<size_t>(u - first);
+        float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
+        for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(wstage + c * 4);
+        if (lane < 4) {
+          if (h0 < g.group) {
+            part_ml[(slot * g.group + h0) * 2] = m0;
+            part_ml[(slot * g.group + h0) * 2 + 1] = lt0;
+          }
+          if (h0 + 1 < g.group) {
+            part_ml[(slot * g.group + h0 + 1) * 2] = m1;
+            part_ml[(slot * g.group + h0 + 1) * 2 + 1] = lt1;
+          }
+        }
+      }
+      __syncwarp();  // the staging holds the next segment's Q next
+    }
+  }
+}
+
+// Folds the unit pieces of sequences split across units (page-major
+// decode): CTA = (sequence, kv head, query head), thread = head dim.
+__global__ void decode_combine_pages_kernel(AttnGeom g, const AttnSeq* __restrict__ seqs,
+                                            const int* __restrict__ seq_prefix, long long total, long long W,
+                                            int max_pieces, const float* __restrict__ part_o,
+                                            const float* __restrict__ part_ml, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int item = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
+  const int hkv = g.n_kv_heads;
+  const int seq = item / hkv, kvh = item % hkv;
+  const long long t0 = seq_prefix[seq], t1 = seq_prefix[seq + 1];
+  const long long first = ((t0 + 1) * W - 1) / total;
+  const long long last = (t1 * W - 1) / total;
+  const int pieces = static_cast<int>(last - first + 1);
+  if (pieces <= 1) return;
+  const size_t slot0 = static_cast<size_t>(item) * max_pieces * g.group + r;
+  float M = -INFINITY;
+  for (int q = 0; q < pieces; ++q) M = fmaxf(M, part_ml[(slot0 + static_cast<size_t>(q) * g.group) * 2]);
+  float acc = 0.f, L = 0.f;
+  for (int q = 0; q < pieces; ++q) {
+    const size_t slot = slot0 + static_cast<size_t>(q) * g.group;
+    const float ms = part_ml[slot * 2];
+    const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
+    L += part_ml[slot * 2 + 1] * w;
+    acc += part_o[slot * kHD + d] * w;
+  }
+  out[static_cast<size_t>(seqs[seq].q_start) * g.out_stride + (kvh * g.group + r) * kHD + d] =
+      __float2bfloat16(L > 0.f ? acc / L : 0.f);
+}
 
 }  // namespace
 
@@ -651,6 +915,9 @@ size_t attn_smem_bytes_pf() {
 size_t attn_smem_bytes_dec() {
   return static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 2 * 8 * kHD * 2) * 2 + kPairsD * kStD * 8 +
          kPairsD * 32 * 4 + 64;
+}
+size_t attn_smem_bytes_dec_pages(int hkv) {
+  return static_cast<size_t>(kStPg) * hkv * kKVBlock * 2 + static_cast<size_t>(hkv) * 8 * kHD * 4 + kStPg * 8 + 64;
 }
 size_t attn_smem_bytes() { return std::max(attn_smem_bytes_pf(), attn_smem_bytes_dec()); }
 
@@ -675,6 +942,27 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (n_seq == 0 || total_tiles == 0) return cudaSuccess;
   if (g.group > 8) return cudaErrorInvalidValue;
   ensure_kernels_prepared();
+  static const bool pairs = [] {  // NX_DEC_ATTN=pairs: the per-(sequence, kv head) warp-pair kernel
+    const char* e = std::getenv("NX_DEC_ATTN");
+    return e && std::string(e) == "pairs";
+  }();
+  if (!pairs && g.n_kv_heads <= 8) {
+    const long long T = total_tiles / g.n_kv_heads;  // 32-key tiles, sequence-major
+    const long long W = std::min<long long>(sm_count, T);
+    const long long per_min = std::max<long long>(1, T / W);
+    const int max_pieces = static_cast<int>((max_seq_tiles + per_min - 1) / per_min) + 1;
+    if (static_cast<size_t>(n_seq) * g.n_kv_heads * max_pieces * g.group * kHD > part_cap)
+      return cudaErrorInvalidValue;
+    const size_t smem = attn_smem_bytes_dec_pages(g.n_kv_heads);
+    ++g_kernel_launches;
+    cudaError_t e = launch_pdl(decode_attn_pages_kernel, dim3(static_cast<unsigned>(W)), dim3(g.n_kv_heads * 32),
+                               smem, s, g, qkv, kplane, seqs, seq_prefix, n_seq, T, W, pages, max_pieces, out,
+                               part_o, part_ml);
+    if (e != cudaSuccess) return e;
+    ++g_kernel_launches;
+    return launch_pdl(decode_combine_pages_kernel, dim3(n_seq * g.n_kv_heads, g.group), dim3(kHD), 0, s, g, seqs,
+                      seq_prefix, T, W, max_pieces, part_o, part_ml, out);
+  }
   const size_t smem = attn_smem_bytes_dec();
   const long long W = std::min<long long>(static_cast<long long>(sm_count) * kPairsD, total_tiles);
   const int grid = static_cast<int>((W + kPairsD - 1) / kPairsD);
@@ -698,7 +986,10 @@ void prepare_attention_kernels() {
                        static_cast<int>(attn_smem_bytes_pf()));
   cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(attn_smem_bytes_dec()));
+  cudaFuncSetAttribute(decode_attn_pages_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(attn_smem_bytes_dec_pages(8)));
   cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, decode_combine_pages_kernel);
   cudaFuncGetAttributes(&fa, decode_combine_kernel);
 }
 
