@@ -41,8 +41,8 @@ constexpr int kThreadsAttn = 128;
 constexpr int kStagesPF = 2;   // prefill: 2 x 32 KB KV stages (+16 KB Q staging)
 
 constexpr int kKVBlock = 2 * 16 * kHD;  // elements of one (page, kv head) K|V block
-// Smem row of key r of a tile of interleaved (page, kv head) blocks.
-__device__ __forceinline__ int kv_row(int r) { return ((r >> 4) << 5) | (r & 15); }
+// Key r of a tile of interleaved (page, kv head) blocks sits at smem row
+// kv_row(r) = 32 (r / 16) + r % 16 of the K view (the V view is 16 rows on).
 
 // Swizzled offset (elements) of (row, col) in a [rows][128] bf16 tile.
 __device__ __forceinline__ int swz(int row, int col) {
@@ -121,6 +121,15 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], uint32_t
                                             float (&l)[2], float (&o)[16][4], float scale_log2,
                                             int key0) {
   const int lane = threadIdx.x & 31;
+  // hoisted ldmatrix lane offsets (see decode_attn_kernel): K rows 2 kb + (lane & 7) + 8 b4,
+  // chunk 2 k + b3; V rows 2 ks 16 + (lane & 7) + 8 b3, chunk 2 d2 + b4
+  const int l7 = lane & 7, b3 = (lane >> 3) & 1, b4 = lane >> 4, gx = (l7 & 6) >> 1;
+  uint32_t koff[4], voff[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    koff[j] = static_cast<uint32_t>((l7 + 8 * b4) * kHD * 2 + (((b3 ^ l7) & 1) << 4) + ((j ^ gx) << 5));
+    voff[j] = static_cast<uint32_t>((l7 + 8 * b3) * kHD * 2 + (((b4 ^ l7) & 1) << 4) + ((j ^ gx) << 5));
+  }
   float s[8][4];
 #pragma unroll
   for (int n = 0; n < 8; ++n)
@@ -134,9 +143,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], uint32_t
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       uint32_t b[4];
-      const int row = kv_row(kb + (lane & 7) + ((lane >> 4) << 3));
-      const int col = k * 16 + (((lane >> 3) & 1) << 3);
-      ldsm_x4_s(b, sk + 2 * swz(row, col));
+      ldsm_x4_s(b, sk + kb * 2 * kHD * 2 + koff[k & 3] + ((k & 4) << 5));  // kv_row(kb + y) = 2 kb + y
       mma16816(s[2 * n2], qf[k], b[0], b[1]);
       mma16816(s[2 * n2 + 1], qf[k], b[2], b[3]);
     }
@@ -204,9 +211,7 @@ __device__ __forceinline__ void attend_tile(const uint32_t (&qf)[8][4], uint32_t
 #pragma unroll
     for (int d2 = 0; d2 < 8; ++d2) {
       uint32_t b[4];
-      const int row = kv_row(ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3));
-      const int col = d2 * 16 + ((lane >> 4) << 3);
-      ldsm_x4_t_s(b, sv + 2 * swz(row, col));
+      ldsm_x4_t_s(b, sv + ks * 32 * kHD * 2 + voff[d2 & 3] + ((d2 & 4) << 5));
       mma16816(o[2 * d2], pf[ks], b[0], b[1]);
       mma16816(o[2 * d2 + 1], pf[ks], b[2], b[3]);
     }
@@ -462,6 +467,19 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   int seg_tile0 = cur.tile;
   const int h0 = 2 * (lane & 3);
   const int krow = half * 16;  // this warp's 16 keys of every tile
+  // ldmatrix lane addresses, hoisted: in the 128B-swizzled rows, chunk (2 k + b)
+  // of a row r sits at ((2 k + b) ^ (r & 7)) << 4 = (b ^ (r & 1)) << 4 | ((k ^ g) << 5)
+  // with g = (r & 6) >> 1, so 4 per-lane bases cover k = 0..7 (k & 4 is an
+  // immediate +128 B). K: row 2 krow + (lane & 7) + 8 b3, chunk b = lane >> 4;
+  // V (trans): row 2 krow + (lane & 7) + 8 (lane >> 4), chunk b = b3.
+  const int l7 = lane & 7, b3 = (lane >> 3) & 1, b4 = lane >> 4, gx = (l7 & 6) >> 1;
+  uint32_t koff[4], voff[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    koff[j] = static_cast<uint32_t>((2 * krow + l7 + 8 * b3) * kHD * 2 + (((b4 ^ l7) & 1) << 4) + ((j ^ gx) << 5));
+    voff[j] = static_cast<uint32_t>((2 * krow + l7 + 8 * b4) * kHD * 2 + 16 * kHD * 2 + (((b3 ^ l7) & 1) << 4) +
+                                    ((j ^ gx) << 5));
+  }
   for (long long gt = lo; gt < hi; ++gt) {
     const int i = static_cast<int>(gt - lo), buf = i % kStD;
     if (gt == lo || cur.tile == 0) {  // new segment: this item's queries
@@ -488,15 +506,14 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
       for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     }
     mbar_wait(&full[buf], (i / kStD) & 1);
-    // [2 blocks][K 16 | V 16][128]; shared-window byte addresses
-    const uint32_t sk = pbase_s + static_cast<uint32_t>(buf * 2 * kTileD * 2);
-    const uint32_t sv = sk + 16 * kHD * 2;
+    // [2 blocks][K 16 | V 16][128]; shared-window byte address of the stage
+    const uint32_t sbase = pbase_s + static_cast<uint32_t>(buf * 2 * kTileD * 2);
     // S^T = K Q^T over this warp's 16 keys: 8 k-steps in two chains
     float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       uint32_t a[4];
-      ldsm_x4_s(a, sk + 2 * swz(2 * krow + (lane & 7) + (((lane >> 3) & 1) << 3), k * 16 + ((lane >> 4) << 3)));
+      ldsm_x4_s(a, sbase + koff[k & 3] + ((k & 4) << 5));
       mma16816((k & 1) ? s2 : s, a, qb[k][0], qb[k][1]);
     }
 #pragma unroll
@@ -536,7 +553,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 #pragma unroll
     for (int db = 0; db < 8; ++db) {
       uint32_t a[4];
-      ldsm_x4_t_s(a, sv + 2 * swz(2 * krow + (lane & 7) + ((lane >> 4) << 3), db * 16 + (((lane >> 3) & 1) << 3)));
+      ldsm_x4_t_s(a, sbase + voff[db & 3] + ((db & 4) << 5));
       mma16816(o[db], a, pb0, pb1);
     }
     pair_sync();  // both warps are done with stage buf
