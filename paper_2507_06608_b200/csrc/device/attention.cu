@@ -356,20 +356,6 @@ constexpr int kPairsD = 4;    // warp pairs per CTA (one CTA per SM)
 constexpr int kWarpsD = 2 * kPairsD;
 constexpr int kTileD = kKTD * kHD;  // elements per K (or V) tile
 
-__device__ __forceinline__ void issue_dec_tile(__nv_bfloat16* sk, __nv_bfloat16* sv, uint64_t* bar,
-                                               const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
-                                               const int32_t* pt, int kv_len, int tile, int kvh,
-                                               const AttnGeom& g, uint64_t policy) {
-  const int last_page = pt[(kv_len - 1) >> 4];
-  mbar_expect_tx(bar, 2 * 2 * 4096);
-#pragma unroll
-  for (int p = 0; p < 2; ++p) {
-    const int key = tile * kKTD + p * 16;
-    const int page = key < kv_len ? pt[key >> 4] : last_page;
-    const size_t off = (static_cast<size_t>(page) * g.n_kv_heads + kvh) * kKVBlock;
-    bulk_load(sk + p * kKVBlock, kplane + off, 8192, bar, policy);  // [K 16 | V 16] block
-  }
-}
 
 // Item (sequence, kv head) holding flattened tile index gt: seq_prefix[s] is
 // the first tile of sequence s (all heads), tiles(s) = ceil(kv_len / 32).
@@ -443,17 +429,36 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   pair_sync();
   pdl_wait();  // the new token's K/V and Q come from the QKV / RoPE kernels
   const uint64_t pol = policy_evict_first();
-  // producer cursor (one lane) runs kStD tiles ahead of the consumer cursor
+  // producer cursor (one lane) runs kStD tiles ahead of the consumer cursor;
+  // the page ids of the next tile to issue are looked up one refill ahead, so
+  // the dependent global loads (sequence -> page table -> page) overlap a tile
+  // of compute instead of stalling the producer's warp at every refill
   DecPos prod = dec_locate(seq_prefix, n_seq, hkv, lo);
   long long issued = lo;
+  int nxt_pg0 = 0, nxt_pg1 = 0, nxt_kvh = 0;
+  auto lookup = [&]() {
+    const AttnSeq ms = seqs[prod.seq];
+    const int32_t* pt = pages + ms.page_off;
+    const int last = pt[(ms.kv_len - 1) >> 4];  // keys past kv_len re-load it (masked, finite)
+    const int key = prod.tile * kKTD;
+    nxt_pg0 = key < ms.kv_len ? pt[key >> 4] : last;
+    nxt_pg1 = key + 16 < ms.kv_len ? pt[(key + 16) >> 4] : last;
+    nxt_kvh = prod.kvh;
+  };
+  auto issue = [&](int st) {
+    __nv_bfloat16* dst = pbase + st * 2 * kTileD;
+    mbar_expect_tx(&full[st], 2 * 2 * 4096);
+    bulk_load(dst, kplane + (static_cast<size_t>(nxt_pg0) * hkv + nxt_kvh) * kKVBlock, 8192, &full[st], pol);
+    bulk_load(dst + kKVBlock, kplane + (static_cast<size_t>(nxt_pg1) * hkv + nxt_kvh) * kKVBlock, 8192, &full[st],
+              pol);
+  };
   if (producer) {
     for (; issued < hi && issued < lo + kStD; ++issued) {
-      const int st = static_cast<int>(issued - lo);
-      const AttnSeq ms = seqs[prod.seq];
-      issue_dec_tile(pbase + st * 2 * kTileD, pbase + st * 2 * kTileD + kTileD, &full[st], kplane,
-                     vplane, pages + ms.page_off, ms.kv_len, prod.tile, prod.kvh, g, pol);
+      lookup();
+      issue(static_cast<int>(issued - lo));
       dec_advance(prod, seq_prefix, n_seq, hkv);
     }
+    if (issued < hi) lookup();
   }
   DecPos cur = dec_locate(seq_prefix, n_seq, hkv, lo);
   // Transposed tile math: S^T = K Q^T and O^T += V^T P^T, so keys / head
@@ -559,11 +564,9 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
     pair_sync();  // both warps are done with stage buf
     // refill this stage kStD tiles ahead
     if (producer && issued < hi) {
-      const AttnSeq ms = seqs[prod.seq];
-      issue_dec_tile(pbase + buf * 2 * kTileD, pbase + buf * 2 * kTileD + kTileD, &full[buf], kplane,
-                     vplane, pages + ms.page_off, ms.kv_len, prod.tile, prod.kvh, g, pol);
+      issue(buf);
       dec_advance(prod, seq_prefix, n_seq, hkv);
-      ++issued;
+      if (++issued < hi) lookup();
     }
     // segment end: last tile of the item or of this unit's range
     const bool item_end = cur.tile == cur.n_tiles - 1;
