@@ -224,16 +224,26 @@ __device__ __forceinline__ void load_q_frag(uint32_t (&qf)[8][4], const __nv_bfl
                                             const AttnGeom& g, int tok_base, int n_tok,
                                             int row0, int kvh, __nv_bfloat16* stage) {
   const int lane = threadIdx.x & 31;
-  // stage 16 x 128 into (swizzled) smem via 16 B loads, then ldmatrix
-  for (int c = lane; c < 16 * 16; c += 32) {
-    const int r = c >> 4, chunk = c & 15;
-    const int gr = row0 + r;
-    const int t = gr / g.group, head = kvh * g.group + gr % g.group;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (t < n_tok)
-      v = *reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(tok_base + t) * g.qkv_stride +
-                                          head * kHD + chunk * 8);
-    *reinterpret_cast<uint4*>(stage + r * kHD + ((chunk ^ (r & 7)) << 3)) = v;
+  // stage 16 x 128 into (swizzled) smem via 16 B loads, then ldmatrix. Lane l
+  // covers chunk l & 15 of rows (l >> 4) + 2 i; all 8 loads are issued before
+  // the first store, and (token, head) of row r advance incrementally (a
+  // per-element division by the group size was 8% of the kernel's instructions).
+  const int chunk = lane & 15;
+  int gr = row0 + (lane >> 4);
+  int t = gr / g.group, hd = gr - t * g.group;
+  uint4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = t < n_tok ? *reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(tok_base + t) * g.qkv_stride +
+                                                        (kvh * g.group + hd) * kHD + chunk * 8)
+                     : make_uint4(0, 0, 0, 0);
+    hd += 2;
+    while (hd >= g.group) hd -= g.group, ++t;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (lane >> 4) + 2 * i;
+    *reinterpret_cast<uint4*>(stage + r * kHD + ((chunk ^ (r & 7)) << 3)) = v[i];
   }
   __syncwarp();
 #pragma unroll
