@@ -26,3 +26,12 @@ for r in range(REPS):
         t0 = time.perf_counter(); dev.launch(P, lane=0, sm_pct=PPCT); t1 = time.perf_counter()
         _, ms = dev.wait(0); t2 = time.perf_counter()
         print(f"prefill device_ms {ms:.3f} host_enqueue_ms {1e3*(t1-t0):.3f} wall_ms {1e3*(t2-t0):.3f}", flush=True)
+    if MODE == "colo":  # prefill on its partition while decode steps run back to back on the other
+        DSTEPS = int(os.environ.get("DSTEPS", "4"))
+        dev.launch(P, lane=0, sm_pct=PPCT)
+        dms = []
+        for _ in range(DSTEPS):
+            dev.launch(Dm, lane=1, sm_pct=DPCT)
+            dms.append(dev.wait(1)[1])
+        _, pms = dev.wait(0)
+        print(f"colo prefill_ms {pms:.3f} decode_ms {sum(dms)/len(dms):.3f} ({DSTEPS} steps)", flush=True)
