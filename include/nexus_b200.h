@@ -594,7 +594,8 @@ int nx_dev_sync(void);
 /* out = epilogue(x[tokens, K] . w[rows, K]^T) with the tcgen05 GEMM; mode is
  * the epilogue (0 store, 1 bias, 2 residual, 3 bias+residual, 4 SwiGLU,
  * 6 fp32; 16 / 17: the decode GEMM (tokens <= 128) with deferred fold /
- * direct, fp32 out). sm_count caps the persistent grid; splits 0 = automatic.
+ * direct, fp32 out). sm_count caps the persistent grid; splits 0 = automatic,
+ * -2 = the CTA-pair (cta_group::2) prefill kernel.
  * Returns the device time of `iters` launches in *ms (may be NULL). */
 /* Diagnostics: per-CTA %globaltimer milestones of the last GEMM launched with
  * NX_GEMM_DBG & 16 set ([cta][8] u64); returns the count copied. */

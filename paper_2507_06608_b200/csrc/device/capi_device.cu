@@ -231,9 +231,14 @@ int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32
                int32_t sm_count, int32_t splits, int32_t iters, float* ms) {
   return dguard([&] {
     if (mode == 16 || mode == 17) return op_gemm_decode(x, w, tokens, rows, K, mode, out, sm_count, iters, ms);
+    const bool pair = splits == -2;  // CTA-pair prefill GEMM (gemm_tc2.cu)
+    if (pair) splits = 0;
     const int bn = nxd::gemm_pick_bn(tokens);
     CUtensorMap xm;
     if (!nxd::encode_kmajor(&xm, x, tokens, K, static_cast<uint64_t>(K) * 2, bn))
+      return dfail(NX_ERUNTIME, "tensor map encode failed");
+    CUtensorMap xm128;
+    if (!nxd::encode_kmajor(&xm128, x, tokens, K, static_cast<uint64_t>(K) * 2, 128))
       return dfail(NX_ERUNTIME, "tensor map encode failed");
     __nv_bfloat16* wp = nullptr;
     int prc = cuda_rc(cudaMalloc(&wp, nxd::packed_weight_elems(rows, K) * 2));
@@ -262,10 +267,13 @@ int nx_op_gemm(const void* x, const void* w, int32_t tokens, int32_t rows, int32
     cudaError_t err = cudaSuccess;
     for (int i = 0; i < n && err == cudaSuccess; ++i) {
       cudaEventRecord(ev[2 * i], nullptr);
-      err = nxd::gemm(wp, xm, bn, rows, tokens, K, mode, out, ldo,
-                      static_cast<const __nv_bfloat16*>(bias),
-                      static_cast<const __nv_bfloat16*>(residual), ldr, ws, ws_bytes, sm_count,
-                      nullptr, splits, /*coresident=*/true);
+      err = pair ? nxd::gemm_pair(wp, xm128, rows, tokens, K, mode, out, ldo,
+                                  static_cast<const __nv_bfloat16*>(bias),
+                                  static_cast<const __nv_bfloat16*>(residual), ldr, sm_count, nullptr)
+                 : nxd::gemm(wp, xm, bn, rows, tokens, K, mode, out, ldo,
+                             static_cast<const __nv_bfloat16*>(bias),
+                             static_cast<const __nv_bfloat16*>(residual), ldr, ws, ws_bytes, sm_count,
+                             nullptr, splits, /*coresident=*/true);
       cudaEventRecord(ev[2 * i + 1], nullptr);
     }
     if (err == cudaSuccess) err = cudaDeviceSynchronize();

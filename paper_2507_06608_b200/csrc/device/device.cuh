@@ -141,6 +141,15 @@ cudaError_t gemm_decode(const __nv_bfloat16* w_packed, const CUtensorMap& x_map,
                         int tokens, int K, float* out, int ldo, float* ws, size_t ws_bytes, int sm_count,
                         cudaStream_t stream, GemmFold* fold);
 void prepare_gemm_decode_kernel();
+// Prefill GEMM on CTA pairs (cta_group::2, gemm_tc2.cu): 256 weight rows x 256
+// tokens per pair, each CTA staging half of the activation tile. x_map128 is
+// the activations' K-major map with 128-row boxes. The forward uses it for every
+// prefill-shaped GEMM unless NX_GEMM_2CTA=0 (gemm_pair_enabled()).
+bool gemm_pair_enabled();
+cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128, int rows, int tokens, int K,
+                      int mode, void* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* residual, int ldr,
+                      int sm_count, cudaStream_t stream);
+void prepare_gemm_pair_kernel();
 constexpr int kGemmMaxCounterTiles = 8192;  // [arrive | depart] int counters
 
 // K-major bf16 [rows, cols] tensor map with a 64 x box_rows, 128B-swizzled box.

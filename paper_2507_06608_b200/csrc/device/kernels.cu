@@ -566,6 +566,7 @@ void ensure_kernels_prepared() {
   if (mask.load() & bit) return;
   prepare_gemm_kernels();
   prepare_gemm_decode_kernel();
+  prepare_gemm_pair_kernel();
   prepare_attention_kernels();
   prepare_tp_kernels();
   const void* fns[] = {reinterpret_cast<const void*>(fill_random_kernel),

@@ -546,6 +546,8 @@ void Model::forward(LaneWs& ws) {
   // each read the fp32 planes, so no GEMM waits on a fix-up round trip and
   // the separate RMSNorm / RoPE launches disappear.
   const bool fold = fold_enabled_ && tp_ == 1 && T <= 128;
+  // prefill-shaped GEMMs on CTA pairs (cta_group::2) when enabled
+  const bool pair = !fold && bn == 256 && sm >= 2 && gemm_pair_enabled();
   GemmFold fq, fo, fg, fd;
   // bytes of the planes a fold reads: pieces <= ~max planes; count one plane
   auto pbytes = [&](double rows) { return Td * rows * 4; };
@@ -561,6 +563,8 @@ void Model::forward(LaneWs& ws) {
       });
     timed(gk, gbytes(qkv_rows_, d, fold ? 4 : 2, false), gflops(qkv_rows_, d), [&] {
       ck(fold ? gemm_decode(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fq)
+              : pair ? gemm_pair(w.qkv, ws.map_h[2], qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore, ws.qkv,
+                                 qkv_rows_, w.qkv_bias, nullptr, 0, sm, s)
               : gemm(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
                      ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "qkv gemm");
@@ -597,6 +601,7 @@ void Model::forward(LaneWs& ws) {
     const int res_mode = (tp_ == 1 || rank_ == 0) ? kEpiResidual : kEpiStore;
     timed(gk, gbytes(d, attn_cols_, fold ? 4 : 2, !fold), gflops(d, attn_cols_), [&] {
       ck(fold ? gemm_decode(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fo)
+              : pair ? gemm_pair(w.o, ws.map_attn[2], d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x, d, sm, s)
               : gemm(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x,
                      d, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "o gemm");
@@ -612,6 +617,8 @@ void Model::forward(LaneWs& ws) {
       });
     timed(gk, gbytes(2.0 * ffn_, d, fold ? 8 : 1, false), gflops(2.0 * ffn_, d), [&] {
       ck(fold ? gemm_decode(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fg)
+              : pair ? gemm_pair(w.gate_up, ws.map_h[2], 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr, nullptr, 0,
+                                 sm, s)
               : gemm(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr,
                      nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "gate/up gemm");
@@ -622,6 +629,7 @@ void Model::forward(LaneWs& ws) {
       });
     timed(gk, gbytes(d, ffn_, fold ? 4 : 2, !fold), gflops(d, ffn_), [&] {
       ck(fold ? gemm_decode(w.down, ws.map_act[bi], bn, d, T, ffn_, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fd)
+              : pair ? gemm_pair(w.down, ws.map_act[2], d, T, ffn_, res_mode, ws.x, d, nullptr, ws.x, d, sm, s)
               : gemm(w.down, ws.map_act[bi], bn, d, T, ffn_, res_mode, ws.x, d, nullptr, ws.x, d,
                      ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "down gemm");

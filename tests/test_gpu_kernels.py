@@ -110,6 +110,30 @@ def test_gemm_decode(D, T, N, K, sms):
         np.testing.assert_allclose(dev, ref, rtol=1e-3, atol=1e-3 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("T,N,K,sms", [(300, 1024, 512, 148), (2048, 4096 + 128, 1024, 116), (700, 2048, 4096, 16)])
+def test_gemm_pair_cta_group2(D, T, N, K, sms):
+    """Prefill GEMM on CTA pairs (tcgen05 cta_group::2): store, residual and
+    SwiGLU epilogues against the fp32 product."""
+    rng = np.random.default_rng(T + N + K)
+    x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
+    r = _rand(D, rng, (T, N))
+    base = D.bf16_to_f32(x) @ D.bf16_to_f32(w).T
+    bx, bw, br = D.Buf.from_array(x), D.Buf.from_array(w), D.Buf.from_array(r)
+    bo = D.Buf(T * N * 2)
+    D.gemm(bx, bw, T, N, K, D.EPI_STORE, bo, N, sm_count=sms, splits=-2)
+    _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), base)
+    D.gemm(bx, bw, T, N, K, D.EPI_RESIDUAL, bo, N, residual=br, ldr=N, sm_count=sms, splits=-2)
+    _close(D.bf16_to_f32(bo.to_array((T, N), np.uint16)), base + D.bf16_to_f32(r))
+    if N % 128 == 0:
+        F = N // 2
+        wf = D.bf16_to_f32(w).reshape(F // 64, 2, 64, K)
+        g = D.bf16_to_f32(x) @ wf[:, 0].reshape(F, K).T
+        u = D.bf16_to_f32(x) @ wf[:, 1].reshape(F, K).T
+        bs = D.Buf(T * F * 2)
+        D.gemm(bx, bw, T, N, K, D.EPI_SWIGLU, bs, F, sm_count=sms, splits=-2)
+        _close(D.bf16_to_f32(bs.to_array((T, F), np.uint16)), g / (1 + np.exp(-g)) * u)
+
+
 def test_gemm_f32_logits(D):
     T, N, K = 40, 1024 * 8, 512
     rng = np.random.default_rng(9)
