@@ -146,6 +146,7 @@ void prepare_gemm_decode_kernel();
 // the activations' K-major map with 128-row boxes. The forward uses it for every
 // prefill-shaped GEMM unless NX_GEMM_2CTA=0 (gemm_pair_enabled()).
 bool gemm_pair_enabled();
+bool gemm_bn_fit_enabled();  // runtime prefill token-tile width (NX_BN_FIT=0: always 256)
 cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128, int rows, int tokens, int K,
                       int mode, void* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* residual, int ldr,
                       int sm_count, cudaStream_t stream);

@@ -788,7 +788,9 @@ cudaError_t launch_bn(const __nv_bfloat16* tw, const CUtensorMap& tx, const Gemm
 }  // namespace
 
 // NX_BN_FIT=0 keeps N = 256 for every prefill tile.
-static bool bn_fit_enabled() {
+bool gemm_bn_fit_enabled();
+static bool bn_fit_enabled() { return gemm_bn_fit_enabled(); }
+bool gemm_bn_fit_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("NX_BN_FIT");
     return !(e && e[0] == '0');

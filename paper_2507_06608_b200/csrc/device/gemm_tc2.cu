@@ -96,6 +96,7 @@ __host__ __device__ __forceinline__ size_t packed_row(int m_blk, int kb, int num
 
 struct Pair2Params {
   int rows, tokens, num_kb, n_pairs, n_nblk;  // n_pairs = 256-row weight pairs
+  int bn;                                     // token tile width N (<= 256, multiple of 16; N / 2 per CTA)
   int mode;
   void* out;
   int ldo;
@@ -119,7 +120,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair_id = blockIdx.x >> 1, n_pair_ctas = gridDim.x >> 1;
-  pdl_trigger();
+  // No programmatic dependent launch for the pair kernel (launched stream-
+  // ordered, no early trigger): with PDL the monolithic bench hung in ~1 of 3
+  // runs (never with NX_PDL=0); the griddepcontrol.wait calls below are then
+  // no-ops.
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tw);
     tma_prefetch(&tx);
@@ -171,7 +175,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (leader) mbar_expect_tx(&full[stage], 2 * kStage);
             tma_2d_pair(&tw, &full[stage], st, 0, static_cast<int>(packed_row(m_blk, kb, p.num_kb)), w_policy);
           }
-          tma_2d_pair(&tx, &full[stage], st + kWBytes, kb * kBK, n_blk * kBN + static_cast<int>(rank) * kHalfN,
+          tma_2d_pair(&tx, &full[stage], st + kWBytes, kb * kBK, n_blk * p.bn + static_cast<int>(rank) * (p.bn >> 1),
                       x_policy);
           if (++stage == kStages) {
             stage = 0;
@@ -183,7 +187,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (CTA 0 of the pair) ----------------
     if (leader) {
-      constexpr uint32_t idesc = umma_idesc_bf16(2 * kBM, kBN);
+      const uint32_t idesc = umma_idesc_bf16(2 * kBM, p.bn);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -227,9 +231,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int n_blk = u % p.n_nblk;
       const int f0 = m128 * kBM;
       const bool valid_rows = f0 < p.rows;
-      for (int c0 = 0; c0 < kBN && valid_rows; c0 += 32) {
-        const int tok0 = n_blk * kBN + c0;
-        if (tok0 >= p.tokens) break;
+      const int tlim = min(p.tokens, (n_blk + 1) * p.bn);  // this tile's token rows
+      for (int c0 = 0; c0 < p.bn && valid_rows; c0 += 32) {
+        const int tok0 = n_blk * p.bn + c0;
+        if (tok0 >= tlim) break;
         const bool has_res = p.mode == kEpiResidual || p.mode == kEpiBiasResidual;
         uint4 res[4];
         if (has_res) {
@@ -237,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int pass = 0; pass < 4; ++pass) {
             const int t = tok0 + pass * 8 + (et >> 4);
-            res[pass] = t < p.tokens ? *reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(t) * p.ldr +
+            res[pass] = t < tlim ? *reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(t) * p.ldr +
                                                                       f0 + g * 8)
                                      : make_uint4(0, 0, 0, 0);
           }
@@ -254,7 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int pass = 0; pass < 2; ++pass) {
             const int j = pass * 16 + (et >> 3);
             const int t = tok0 + j;
-            if (t < p.tokens) {
+            if (t < tlim) {
               __align__(16) __nv_bfloat16 o[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i)
@@ -269,7 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int pass = 0; pass < 8; ++pass) {
             const int j = pass * 4 + (et >> 5);
             const int t = tok0 + j;
-            if (t < p.tokens)
+            if (t < tlim)
               *reinterpret_cast<float4*>(static_cast<float*>(p.out) + static_cast<size_t>(t) * p.ldo + f0 + g * 4) =
                   *reinterpret_cast<const float4*>(&s_epi[j * kBM + g * 4]);
           }
@@ -279,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int pass = 0; pass < 4; ++pass) {
             const int j = pass * 8 + (et >> 4);
             const int t = tok0 + j;
-            if (t < p.tokens) {
+            if (t < tlim) {
               float v[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) v[i] = s_epi[j * kBM + g * 8 + i];
@@ -354,7 +359,19 @@ cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128
   p.tokens = tokens;
   p.num_kb = K / kBK;
   p.n_pairs = (rows / kBM + 1) / 2;
-  p.n_nblk = (tokens + kBN - 1) / kBN;
+  // token tile width fitted to the pair waves of the partition (as gemm() does
+  // for the single-CTA kernel); N / 2 rows per CTA stay a multiple of 8
+  p.bn = kBN;
+  const int n_pair_slots = std::max(1, sm_count / 2);
+  if (gemm_bn_fit_enabled()) {
+    long long best = -1;
+    for (int n = kBN; n >= 192; n -= 16) {
+      const long long t = static_cast<long long>(p.n_pairs) * ((tokens + n - 1) / n);
+      const long long cost = (t + n_pair_slots - 1) / n_pair_slots * (std::max(n, 208) + 256);
+      if (best < 0 || cost < best) best = cost, p.bn = n;
+    }
+  }
+  p.n_nblk = (tokens + p.bn - 1) / p.bn;
   p.mode = mode;
   p.out = out;
   p.ldo = ldo;
@@ -368,7 +385,8 @@ cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128
   const int pairs = std::max(1, std::min(units, sm_count / 2));
   ensure_kernels_prepared();
   ++g_kernel_launches;
-  return launch_pdl(gemm_tc2_kernel, dim3(2 * pairs), dim3(kThreads), kSmem, stream, tw, x_map128, p);
+  gemm_tc2_kernel<<<dim3(2 * pairs), dim3(kThreads), kSmem, stream>>>(tw, x_map128, p);
+  return cudaGetLastError();
 }
 
 void prepare_gemm_pair_kernel() {

@@ -35,3 +35,7 @@ for r in range(REPS):
             dms.append(dev.wait(1)[1])
         _, pms = dev.wait(0)
         print(f"colo prefill_ms {pms:.3f} decode_ms {sum(dms)/len(dms):.3f} ({DSTEPS} steps)", flush=True)
+    if MODE == "mixed":  # one fused batch (decode members first), monolithic-style full-GPU lane
+        t0 = time.perf_counter(); dev.launch(Dm + P, lane=0, sm_pct=100)
+        _, ms = dev.wait(0); t2 = time.perf_counter()
+        print(f"mixed device_ms {ms:.3f} wall_ms {1e3*(t2-t0):.3f} tokens {len(Dm) + sum(PLENS)}", flush=True)
