@@ -52,9 +52,10 @@ def test_gemm_splits_and_small_grids(D, T, N, K, splits, sms):
 
 
 @pytest.mark.parametrize("T,N,K,sms", [(1024, 4096, 1024, 112), (2048, 6144, 512, 148), (700, 4096, 512, 40)])
-def test_gemm_prefill_hybrid_streamk(D, T, N, K, sms):
-    """Prefill shapes whose last wave is partial: whole waves data-parallel,
-    the remainder stream-K with the in-kernel fix-up (residual epilogue)."""
+def test_gemm_prefill_partial_waves(D, T, N, K, sms):
+    """Prefill shapes whose last wave is partial on the partition: the runtime
+    token-tile width (N in [192, 256]) refits the tiles to the waves
+    (residual epilogue; the hybrid stream-K path runs with NX_HYBRID_FRAC)."""
     rng = np.random.default_rng(T + sms)
     x, w = _rand(D, rng, (T, K)), _rand(D, rng, (N, K), 1 / np.sqrt(K))
     r = _rand(D, rng, (T, N))
