@@ -79,15 +79,33 @@ def parse():
                    help="ControllerConfig.beta, the decode slack in prefill-prioritized mode. The paper's "
                         "1.1 was set for L20; on B200 a 2.0x slack still keeps p99 TBT well inside the "
                         "50 ms SLO (profiles/r01_beta_sweep.md)")
-    p.add_argument("--gamma", type=float, default=1500.0,
+    p.add_argument("--gamma", type=float, default=5000.0,
                    help="ControllerConfig.gamma (SPF aging, tokens of priority per second waited; reference "
-                        "default 15). At 128 rps on B200 with the CTA-pair prefill GEMMs, gamma 1500 lifts goodput "
-                        "10145 -> 10552 tok/s and cuts p99 TTFT 2.67 -> 1.03 s (profiles/r01s2_gamma_*.json); "
-                        "the oracle / reference arm run with the same gamma")
+                        "default 15). At 128 rps on B200 with the CTA-pair prefill GEMMs: gamma 15 -> 10145 tok/s "
+                        "goodput, p99 TTFT 2.67 s; 1500 -> 10552, 1.03 s; 5000 -> 10669, 0.71 s "
+                        "(profiles/r01s2_gamma_*.json); the reference arm runs with the same gamma")
     p.add_argument("--alpha", type=float, default=1.3, help="ControllerConfig.alpha (prefill slack, paper 1.3)")
     p.add_argument("--max-decode-batch", type=int, default=128,
                    help="ControllerConfig.max_decode_batch (reference default 64, domain.hpp:87)")
     return p.parse_args()
+
+
+def partition_roofline(dom, c, pk):
+    sms = c.get("mean_partition_sms", 0.0)
+    if not sms:
+        return None
+    mhz = pk.get("sm_max_mhz", 1965.0)
+    if dom in ("gemm_prefill", "attn_prefill"):
+        ceil = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * sms / 148.0
+        return {"mean_sms": sms, "ceiling": ceil, "unit": "TFLOP/s", "frac": c["TFLOPs"] / ceil,
+                "ceiling_rule": "sustained bf16 peak x mean SMs / 148"}
+    if dom == "gemm_decode":
+        ceil = min(pk["hbm_gbs"], sms * 64 * mhz * 1e6 / 1e9)
+        return {"mean_sms": sms, "ceiling": ceil, "unit": "GB/s", "frac": c["GBps"] / ceil,
+                "ceiling_rule": "min(HBM peak, mean SMs x 64 B/cycle x max SM clock)"}
+    ceil = pk["hbm_gbs"] * min(1.0, sms / 148.0 * 2.0)
+    return {"mean_sms": sms, "ceiling": ceil, "unit": "GB/s", "frac": c["GBps"] / ceil,
+            "ceiling_rule": "HBM peak (reachable from ~half the SMs)"}
 
 
 def peaks():
@@ -370,7 +388,8 @@ def main():
             classes[n] = {"ms_total_sampled": ks.ms[i], "launches_sampled": ks.launches[i],
                           "GBps": ks.bytes[i] / ks.ms[i] / 1e6 if ks.ms[i] else 0.0,
                           "TFLOPs": ks.flops[i] / ks.ms[i] / 1e9 if ks.ms[i] else 0.0,
-                          "avg_launch_ms": per_ms}
+                          "avg_launch_ms": per_ms,
+                          "mean_partition_sms": ks.sm_ms[i] / ks.ms[i] if ks.ms[i] else 0.0}
     dom = max(classes, key=lambda n: classes[n]["ms_total_sampled"]) if classes else None
     roof = None
     if dom:
@@ -396,6 +415,10 @@ def main():
                 "traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "algorithmic_per_launch": (ks.flops[i] if tensor else ks.bytes[i]) / ks.launches[i],
+                # the launches ran on green-context partitions: the HBM peak is not
+                # reachable by a decode GEMM on a few dozen SMs, whose per-SM ceiling
+                # is 64 B of weights per cycle (tcgen05 M = 128 floor, profiles/r01s2_mma_probe.md)
+                "partition": partition_roofline(dom, c, pk),
                 "share_of_sampled_device_time": ks.ms[i] / ks.batch_ms_sampled if ks.batch_ms_sampled else None}
     if rank != 0:
         return

@@ -580,6 +580,7 @@ typedef struct nx_kernel_stats {
   double batch_ms_sampled; /* whole-batch device time of the sampled batches */
   uint64_t kernel_launches; /* every kernel this device launched (all batches) */
   uint64_t batches;         /* every batch this device ran */
+  double sm_ms[NX_K_CLASSES]; /* sum of (lane SM count x event ms): / ms = mean partition size */
 } nx_kernel_stats;
 int nx_device_set_profiling(nx_device* dev, int32_t sample_every);
 int nx_device_kernel_stats(const nx_device* dev, nx_kernel_stats* out);

@@ -727,6 +727,7 @@ void Model::finish(LaneWs& ws) {
       float t = 0.f;
       cudaEventElapsedTime(&t, r.a, r.b);
       kstats_.ms[r.kind] += t;
+      kstats_.sm_ms[r.kind] += t * ws.sm_count;
       kstats_.bytes[r.kind] += r.bytes;
       kstats_.flops[r.kind] += r.flops;
       kstats_.launches[r.kind] += 1;
