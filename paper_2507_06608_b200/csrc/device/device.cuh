@@ -56,6 +56,7 @@ enum EpiMode {
   kEpiSwiGLU = 4,        // out[f] = silu(acc[gate f]) * acc[up f]  (interleaved 64-row blocks)
   kEpiPartial = 5,       // internal: fp32 K-split partials
   kEpiF32 = 6,           // out = acc (fp32), e.g. logits
+  kEpiRopeKV = 7,        // QKV: bf16(acc + bias) -> RoPE on q / k; q -> out, k / v -> paged cache (pair kernel)
 };
 
 struct GemmParams {
@@ -147,9 +148,18 @@ void prepare_gemm_decode_kernel();
 // prefill-shaped GEMM unless NX_GEMM_2CTA=0 (gemm_pair_enabled()).
 bool gemm_pair_enabled();
 bool gemm_bn_fit_enabled();  // runtime prefill token-tile width (NX_BN_FIT=0: always 256)
+// kEpiRopeKV: the QKV projection's epilogue also applies RoPE and writes k / v
+// into the paged cache (`rope` describes it), so no separate RoPE kernel runs.
+struct RopeKV {
+  const int32_t* slot = nullptr;   // per token: page * page_tokens + offset
+  const float2* table = nullptr;   // [tokens][64] (cos, sin)
+  __nv_bfloat16* kplane = nullptr; // layer K view ([page][kv head][K | V][page_tokens][128])
+  __nv_bfloat16* vplane = nullptr; // layer V view (kplane + page_tokens * 128)
+  int n_heads = 0, n_kv_heads = 0, page_tokens = 16;
+};
 cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128, int rows, int tokens, int K,
                       int mode, void* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* residual, int ldr,
-                      int sm_count, cudaStream_t stream);
+                      int sm_count, cudaStream_t stream, const RopeKV* rope = nullptr);
 void prepare_gemm_pair_kernel();
 constexpr int kGemmMaxCounterTiles = 8192;  // [arrive | depart] int counters
 

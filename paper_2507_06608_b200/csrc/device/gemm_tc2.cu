@@ -103,6 +103,8 @@ struct Pair2Params {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* residual;
   int ldr;
+  RopeKV rope;
+  int wpol;  // weight-stream L2 policy: 0 evict_first, 1 evict_normal (default; NX_PAIR_WPOL)
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -151,7 +153,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
-      const uint64_t w_policy = policy_evict_first();
+      uint64_t w_policy = policy_evict_first();
+      if (p.wpol == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(w_policy));
       const uint64_t x_policy = policy_evict_last();
       int stage = 0, fill = 0, pre = 0;
       uint32_t phase = 0;
@@ -253,7 +256,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) s_epi[j * kBM + q * 32 + lane] = __uint_as_float(r[j]);
         named_bar_sync(1, kEpiThreads);
-        if (p.mode == kEpiSwiGLU) {
+        if (p.mode == kEpiRopeKV) {
+          // tile rows = one head: q heads rotate into the qkv output, k heads rotate
+          // into the paged cache, v heads are copied into it (as rope_kv_token)
+          const RopeKV& rk = p.rope;
+          const int head = m128, nq = rk.n_heads, nkv = rk.n_kv_heads;
+          const bool is_v = head >= nq + nkv;
+          auto rnd = [&](int j, int f) {  // bf16(acc + bias) as the unfused GEMM stored it
+            float v = s_epi[j * kBM + f];
+            if (p.bias) v += bf2f(p.bias[f0 + f]);
+            return bf2f(__float2bfloat16(v));
+          };
+          if (!is_v) {
+#pragma unroll
+            for (int pass = 0; pass < 2; ++pass) {
+              const int item = pass * kEpiThreads + et;  // 32 tokens x 8 groups of 8 pairs
+              const int j = item >> 3, grp = item & 7;
+              const int t = tok0 + j;
+              if (t < tlim) {
+                const float2* cs = rk.table + static_cast<size_t>(t) * 64 + grp * 8;
+                __align__(16) __nv_bfloat16 ra[8], rb[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float x = rnd(j, grp * 8 + i), y = rnd(j, 64 + grp * 8 + i);
+                  const float2 c = cs[i];
+                  ra[i] = __float2bfloat16(x * c.x - y * c.y);
+                  rb[i] = __float2bfloat16(y * c.x + x * c.y);
+                }
+                if (head < nq) {
+                  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(t) * p.ldo + f0;
+                  *reinterpret_cast<uint4*>(dst + grp * 8) = *reinterpret_cast<uint4*>(ra);
+                  *reinterpret_cast<uint4*>(dst + 64 + grp * 8) = *reinterpret_cast<uint4*>(rb);
+                } else {
+                  const int sl = rk.slot[t], page = sl / rk.page_tokens, off = sl % rk.page_tokens, sw = off & 7;
+                  __nv_bfloat16* dst =
+                      rk.kplane + ((static_cast<size_t>(page) * nkv + (head - nq)) * 2 * rk.page_tokens + off) * kBM;
+                  *reinterpret_cast<uint4*>(dst + ((grp ^ sw) << 3)) = *reinterpret_cast<uint4*>(ra);
+                  *reinterpret_cast<uint4*>(dst + (((grp + 8) ^ sw) << 3)) = *reinterpret_cast<uint4*>(rb);
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int pass = 0; pass < 4; ++pass) {
+              const int item = pass * kEpiThreads + et;  // 32 tokens x 16 chunks of 8
+              const int j = item >> 4, c = item & 15;
+              const int t = tok0 + j;
+              if (t < tlim) {
+                __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(rnd(j, c * 8 + i));
+                const int sl = rk.slot[t], page = sl / rk.page_tokens, off = sl % rk.page_tokens;
+                __nv_bfloat16* dst =
+                    rk.vplane + ((static_cast<size_t>(page) * nkv + (head - nq - nkv)) * 2 * rk.page_tokens + off) * kBM;
+                *reinterpret_cast<uint4*>(dst + ((c ^ (off & 7)) << 3)) = *reinterpret_cast<uint4*>(o);
+              }
+            }
+          }
+        } else if (p.mode == kEpiSwiGLU) {
           const int g = et & 7;
 #pragma unroll
           for (int pass = 0; pass < 2; ++pass) {
@@ -352,8 +412,10 @@ bool gemm_pair_enabled() {  // NX_GEMM_2CTA=0 falls back to the single-CTA kerne
 
 cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128, int rows, int tokens, int K,
                       int mode, void* out, int ldo, const __nv_bfloat16* bias, const __nv_bfloat16* residual, int ldr,
-                      int sm_count, cudaStream_t stream) {
+                      int sm_count, cudaStream_t stream, const RopeKV* rope) {
   if (rows % kBM || K % kBK || sm_count < 2) return cudaErrorInvalidValue;
+  if (mode == kEpiRopeKV && (rope == nullptr || rows != (rope->n_heads + 2 * rope->n_kv_heads) * kBM))
+    return cudaErrorInvalidValue;
   Pair2Params p{};
   p.rows = rows;
   p.tokens = tokens;
@@ -378,6 +440,15 @@ cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128
   p.bias = bias;
   p.residual = residual;
   p.ldr = ldr;
+  if (rope) p.rope = *rope;
+  // evict_normal for the weight stream: with evict_first the 8 token blocks of a
+  // prefill GEMM re-read each weight tile from DRAM (gate_up T = 2048: 390 MB vs
+  // 262 MB with evict_normal, same time; ncu), DRAM the co-located decode lane needs
+  static const int wpol = [] {
+    const char* e = std::getenv("NX_PAIR_WPOL");
+    return e ? std::atoi(e) : 1;
+  }();
+  p.wpol = wpol;
   CUtensorMap tw;
   const size_t rows64 = packed_weight_elems(rows, K) / 64;
   if (!encode_packed_w(&tw, w_packed, rows64)) return cudaErrorInvalidValue;

@@ -557,19 +557,29 @@ void Model::forward(LaneWs& ws) {
     // per (page, kv head)); the V view starts one K half-block on
     __nv_bfloat16* kplane = kv_ + (2 * static_cast<size_t>(l)) * plane_elems_;
     __nv_bfloat16* vplane = kplane + static_cast<size_t>(cfg_.page_tokens) * a_.head_dim;
+    RopeKV rope;
+    rope.slot = ws.d_slot;
+    rope.table = ws.rope_cs;
+    rope.kplane = kplane;
+    rope.vplane = vplane;
+    rope.n_heads = hq_;
+    rope.n_kv_heads = hkv_;
+    rope.page_tokens = cfg_.page_tokens;
     if (!fold || l == 0)
       timed(NX_K_OTHER, Td * d * 4, 0, [&] {
         ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
       });
     timed(gk, gbytes(qkv_rows_, d, fold ? 4 : 2, false), gflops(qkv_rows_, d), [&] {
       ck(fold ? gemm_decode(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fq)
-              : pair ? gemm_pair(w.qkv, ws.map_h[2], qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore, ws.qkv,
-                                 qkv_rows_, w.qkv_bias, nullptr, 0, sm, s)
+              : pair ? gemm_pair(w.qkv, ws.map_h[2], qkv_rows_, T, d, kEpiRopeKV, ws.qkv, qkv_rows_, w.qkv_bias,
+                                 nullptr, 0, sm, s, &rope)
               : gemm(w.qkv, ws.map_h[bi], bn, qkv_rows_, T, d, w.qkv_bias ? kEpiBias : kEpiStore,
                      ws.qkv, qkv_rows_, w.qkv_bias, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, 0, ws.exclusive),
          "qkv gemm");
     });
-    if (fold)
+    if (pair) {
+      // RoPE + paged KV write ran in the QKV epilogue
+    } else if (fold)
       timed(NX_K_OTHER, pbytes(qkv_rows_) + Td * qkv_rows_ * 2, 0, [&] {
         ck(fold_rope_kv(fq, w.qkv_bias, ws.qkv, ws.d_slot, ws.rope_cs, hq_, hkv_, cfg_.page_tokens, kplane,
                         vplane, s),
