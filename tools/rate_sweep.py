@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--requests", type=int, default=400)
     ap.add_argument("--engines", default="nexus,static,monolithic")
     ap.add_argument("--beta", type=float, default=2.0)
+    ap.add_argument("--gamma", type=float, default=5000.0, help="SPF aging (bench.py default)")
     ap.add_argument("--max-decode-batch", type=int, default=128)
     ap.add_argument("--kv-gb", type=float, default=80.0)
     ap.add_argument("--slo-ttft", type=float, default=1.0)
@@ -46,7 +47,7 @@ def main():
 
     def serve(engine, rate, seed):
         cfg = bench.make_cfg(nx, engine, num_pages, page, nx.NX_CLOCK_DEVICE, calib, True,
-                             args.max_decode_batch, 1.3, args.beta, args.model)
+                             args.max_decode_batch, 1.3, args.beta, args.model, args.gamma)
         trace = nx.workload_trace(args.workload, rate, args.requests, seed)
         rng = np.random.default_rng(seed)
         eng = nx.Engine(cfg, device=dev)
@@ -74,7 +75,7 @@ def main():
         for r in rows:
             f.write(json.dumps(r) + "\n")
     lines = [f"# Rate sweep: {args.model}, {args.workload}, {args.requests} requests per point, "
-             f"SLO TTFT <= {args.slo_ttft}s & p99 TBT <= {1000 * args.slo_tbt:.0f} ms, beta {args.beta}, "
+             f"SLO TTFT <= {args.slo_ttft}s & p99 TBT <= {1000 * args.slo_tbt:.0f} ms, beta {args.beta}, gamma {args.gamma:g}, "
              f"max decode batch {args.max_decode_batch}", "",
              "| rate | engine | goodput tok/s | SLO attain | TTFT p50/p99 ms | TBT p50/p99 ms |",
              "|---|---|---|---|---|---|"]
