@@ -423,7 +423,10 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   float* stage_b = stage_a + 8 * kHD;                       // [8][128] fp32, warp 1
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(smem_attn) +
                                                kPairsD * kPairElems) + pair * kStD;
-  float* ml_b = reinterpret_cast<float*>(full + kPairsD * kStD - pair * kStD) + pair * 32;  // [8 heads][m, l]
+  // empty[s]: both warps of the pair are done reading stage s (2 arrivals); only
+  // the producer waits on it, so neither warp stalls on the other per tile
+  uint64_t* empty = full + kPairsD * kStD;
+  float* ml_b = reinterpret_cast<float*>(full + 2 * kPairsD * kStD - pair * kStD) + pair * 32;  // [8 heads][m, l]
   const uint32_t bar_id = 1 + pair;
   auto pair_sync = [&] { named_bar_sync(bar_id, 64); };
   pdl_trigger();
@@ -433,7 +436,10 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   const int hkv = g.n_kv_heads;
   const bool producer = half == 0 && lane == 0;
   if (producer) {
-    for (int i = 0; i < kStD; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < kStD; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 2);
+    }
     fence_barrier_init();
   }
   pair_sync();
@@ -571,9 +577,11 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
       ldsm_x4_t_s(a, sbase + voff[db & 3] + ((db & 4) << 5));
       mma16816(o[db], a, pb0, pb1);
     }
-    pair_sync();  // both warps are done with stage buf
-    // refill this stage kStD tiles ahead
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with stage buf
+    // refill this stage kStD tiles ahead, once both warps released it
     if (producer && issued < hi) {
+      mbar_wait(&empty[buf], static_cast<uint32_t>((i / kStD) & 1));
       issue(buf);
       dec_advance(prod, seq_prefix, n_seq, hkv);
       if (++issued < hi) lookup();
@@ -943,7 +951,7 @@ size_t attn_smem_bytes_pf() {
   return static_cast<size_t>(2 * kStagesPF * kKT * kHD + 4 * 16 * kHD) * 2 + 64;
 }
 size_t attn_smem_bytes_dec() {
-  return static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 2 * 8 * kHD * 2) * 2 + kPairsD * kStD * 8 +
+  return static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 2 * 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
          kPairsD * 32 * 4 + 64;
 }
 size_t attn_smem_bytes_dec_pages(int hkv) {
