@@ -530,15 +530,19 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
     // [2 blocks][K 16 | V 16][128]; shared-window byte address of the stage
     const uint32_t sbase = pbase_s + static_cast<uint32_t>(buf * 2 * kTileD * 2);
     // S^T = K Q^T over this warp's 16 keys: 8 k-steps in two chains
-    float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+    // four independent accumulation chains of two MMAs (HMMA latency, not issue, bounds a chain)
+    float sc[4][4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sc[c][0] = sc[c][1] = sc[c][2] = sc[c][3] = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       uint32_t a[4];
       ldsm_x4_s(a, sbase + koff[k & 3] + ((k & 4) << 5));
-      mma16816((k & 1) ? s2 : s, a, qb[k][0], qb[k][1]);
+      mma16816(sc[k & 3], a, qb[k][0], qb[k][1]);
     }
+    float s[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) s[j] += s2[j];
+    for (int j = 0; j < 4; ++j) s[j] = (sc[0][j] + sc[1][j]) + (sc[2][j] + sc[3][j]);
     // mask keys past kv_len; online softmax down each head column
     const int key0 = cur.tile * kKTD + krow + (lane >> 2);
     float mx0 = m0, mx1 = m1;
