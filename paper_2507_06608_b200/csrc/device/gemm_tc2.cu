@@ -122,10 +122,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair_id = blockIdx.x >> 1, n_pair_ctas = gridDim.x >> 1;
-  // No programmatic dependent launch for the pair kernel (launched stream-
-  // ordered, no early trigger): with PDL the monolithic bench hung in ~1 of 3
-  // runs (never with NX_PDL=0); the griddepcontrol.wait calls below are then
-  // no-ops.
+  // No early griddepcontrol.launch_dependents: with it (and the kernel launched
+  // with PDL) the monolithic bench hung in ~1 of 3 runs, never with NX_PDL=0.
+  // Launched with PDL but without the trigger (NX_PAIR_PDL=1) it ran 6 of 6
+  // and saves <1% per prefill step, so the default launch is stream-ordered
+  // and the griddepcontrol.wait calls below are no-ops.
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tw);
     tma_prefetch(&tx);
@@ -456,6 +457,14 @@ cudaError_t gemm_pair(const __nv_bfloat16* w_packed, const CUtensorMap& x_map128
   const int pairs = std::max(1, std::min(units, sm_count / 2));
   ensure_kernels_prepared();
   ++g_kernel_launches;
+  // NX_PAIR_PDL=1 (experiment): launch with programmatic serialization so the
+  // prologue and weight prefetch overlap the previous kernel, still without an
+  // early trigger for the kernels after it
+  static const bool pdl = [] {
+    const char* e = std::getenv("NX_PAIR_PDL");
+    return e && e[0] == '1';
+  }();
+  if (pdl) return launch_pdl(gemm_tc2_kernel, dim3(2 * pairs), dim3(kThreads), kSmem, stream, tw, x_map128, p);
   gemm_tc2_kernel<<<dim3(2 * pairs), dim3(kThreads), kSmem, stream>>>(tw, x_map128, p);
   return cudaGetLastError();
 }
