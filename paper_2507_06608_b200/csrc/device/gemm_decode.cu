@@ -59,6 +59,7 @@ struct DecParams {
   uint32_t x_bytes;                   // bytes of one X box (box rows x 128 B)
   int stages;
   uint32_t stage_bytes;               // 32 KB + x_bytes rounded up to 1 KB
+  int prefetch;                       // L2 prefetch distance in k-blocks past the ring (stream-K)
 };
 
 struct DecWork {
@@ -138,6 +139,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto w_src = [&](int tile, int kb) {
         return wpack + (static_cast<size_t>(tile) * p.num_kb + kb) * (kRowsBlk * kKB);
       };
+      // L2 prefetch ahead of the ring: a stream-K CTA's weight range is one
+      // contiguous run ([lo, hi) iterations x 32 KB in the packed layout), so
+      // the chunk kPrefetch iterations past the one being loaded is prefetched
+      // into L2 and the ring's bulk copies see L2 instead of HBM latency (the
+      // ring holds <= 5 x 32 KB per SM: at ~1.5 us loaded HBM latency that caps
+      // a partition-sized grid near 100 GB/s/SM).
+      const long long it_lo = p.streamk ? p.total * blockIdx.x / gridDim.x : 0;
+      const long long it_hi = p.streamk ? p.total * (blockIdx.x + 1) / gridDim.x : 0;
+      auto prefetch = [&](long long it) {
+        if (p.prefetch > 0 && it < it_hi)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wpack + it * (kRowsBlk * kKB)),
+                       "r"(kWBytes)
+                       : "memory");
+      };
+      for (long long it = it_lo + kStages; it < it_lo + kStages + p.prefetch; ++it) prefetch(it);
       // weights of the first kStages stages do not depend on the upstream
       // kernel: stream them before the grid dependency resolves (PDL)
       int pre = 0;
@@ -162,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], kWBytes + p.x_bytes);
             bulk_load(st, w_src(w.tile, kb), kWBytes, &full[stage], w_policy);
+            prefetch(it_lo + fill + kStages + p.prefetch);
           }
           tma_load_2d(&tx, &full[stage], st + kWBytes, kb * kKB, 0);
           if (++stage == kStages) {
@@ -261,6 +278,11 @@ cudaError_t gemm_decode(const __nv_bfloat16* w_packed, const CUtensorMap& x_map,
   p.total = static_cast<long long>(p.n_tiles) * p.num_kb;
   p.x_bytes = static_cast<uint32_t>(box_rows) * kKB * 2;
   p.stage_bytes = kWBytes + ((p.x_bytes + 1023u) & ~1023u);
+  static const int prefetch_kb = [] {
+    const char* e = std::getenv("NX_DEC_PREFETCH");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  p.prefetch = prefetch_kb;
   p.stages = std::min<int>(kStagesMax, (kSmemBudget - 512 - (kXBytes - static_cast<int>(p.x_bytes))) /
                                           static_cast<int>(p.stage_bytes));
   const size_t smem = 1024 + static_cast<size_t>(p.stages) * p.stage_bytes + (kXBytes - p.x_bytes) + 512;
