@@ -17,7 +17,14 @@ for n in PLENS:
     P.append(dict(tokens=rng.integers(0, 1000, n).tolist(), start=0, pages=list(range(pg0, pg0 + n // 16 + 1))))
     pg0 += n // 16 + 1
 import time
+import ctypes
+# ncu --profile-from-start off --replay-mode app-range: profile only the last
+# repetition (RANGE=1), bracketed by cuProfilerStart/Stop
+RANGE = os.environ.get("RANGE", "0") == "1"
+_cuda = ctypes.CDLL("libcuda.so.1") if RANGE else None
 for r in range(REPS):
+    if RANGE and r == REPS - 1:
+        _cuda.cuProfilerStart()
     if MODE in ("decode", "both"):
         t0 = time.perf_counter(); dev.launch(Dm, lane=1, sm_pct=DPCT); t1 = time.perf_counter()
         _, ms = dev.wait(1); t2 = time.perf_counter()
@@ -39,3 +46,5 @@ for r in range(REPS):
         t0 = time.perf_counter(); dev.launch(Dm + P, lane=0, sm_pct=100)
         _, ms = dev.wait(0); t2 = time.perf_counter()
         print(f"mixed device_ms {ms:.3f} wall_ms {1e3*(t2-t0):.3f} tokens {len(Dm) + sum(PLENS)}", flush=True)
+    if RANGE and r == REPS - 1:
+        _cuda.cuProfilerStop()
