@@ -20,11 +20,18 @@ def main(base):
     gpu = nx.gpu_spec(gs["total_sm"], gs["peak_compute"], gs["peak_bandwidth"], 150 << 30)
     prof, _ = nx.parse_kernel_profile(open(base + ".calib").read())
     nx.set_cost_ext(cal["bw_sat"])
+    try:
+        report(cal, m, gpu, prof)
+    finally:
+        nx.set_cost_ext(None)  # process-wide switch: leave the reference form on
+
+
+def report(cal, m, gpu, prof):
     b = cal["batches"]
     dops = nx.decode_op_workloads(m, [b["decode_ctx"]] * b["decode_batch"])
     pops = nx.prefill_batch_workloads(m, [(n, n) for n in b["prefill_chunks"]])
     total = cal["sm_count"]
-    print(f"# Contention refit report: {cal['model']} ({base}.json)\n")
+    print(f"# Contention refit report: {cal['model']} (profiles/b200_{cal['model'].replace('.', '_').replace('-', '_')}.json)\n")
     print("Decode batch B = %d x ctx %d beside a prefill batch of %s tokens; model = the reference"
           % (b["decode_batch"], b["decode_ctx"], "+".join(map(str, b["prefill_chunks"]))))
     print("contended-decode formula (B_decode, costmodel.cpp:56-96) on the refit spec with the")
@@ -38,7 +45,6 @@ def main(base):
         co = nx.decode_latency_contended(dops, sd, pbd, pops, gpu, prof).total_s
         print(f"| {c['decode_sms']} | {c['prefill_sms']} | {c['decode_alone_ms']:.2f} | {c['decode_colocated_ms']:.2f} | "
               f"{c['slowdown']:.3f} | {1e3 * alone:.2f} | {1e3 * co:.2f} | {co / alone:.3f} |")
-    nx.set_cost_ext(None)
 
 
 if __name__ == "__main__":
