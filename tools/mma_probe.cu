@@ -16,7 +16,7 @@ constexpr int kChainsMax = 4;
 constexpr int kA = 128 * 64 * 2;  // 16 KB: 128 rows x 64 K
 constexpr int kB = 256 * 64 * 2;  // 32 KB: up to 256 rows x 64 K
 
-__global__ void __launch_bounds__(128, 1) probe(int n, int chains, int interleave, int rounds,
+__global__ void __launch_bounds__(128, 1) probe(int m, int n, int chains, int interleave, int rounds,
                                                  unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(128, 1) probe(int n, int chains, int interleav
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t idesc = umma_idesc_bf16(128, n);
+  const uint32_t idesc = umma_idesc_bf16(m, n);
   unsigned long long t0 = 0, t1 = 0;
   if (threadIdx.x == 0) {
     t0 = clock64();
@@ -75,12 +75,13 @@ int main(int argc, char** argv) {
   cudaMalloc(&d, 1024 * 8);
   unsigned long long h[1024];
   const int rounds = 256;
+  for (int m : {128, 64})
   for (int n : {32, 64, 128, 160, 192, 208, 224, 240, 256})
     for (int chains : {1, 2, 4})
       for (int il : {0, 1}) {
-        if (chains * n > 512 || (chains == 1 && il)) continue;
-        probe<<<sms, 128, smem>>>(n, chains, il, rounds, d);
-        probe<<<sms, 128, smem>>>(n, chains, il, rounds, d);
+        if (chains * n > 512 || (chains == 1 && il) || (m == 64 && (chains > 1 || n % 64))) continue;
+        probe<<<sms, 128, smem>>>(m, n, chains, il, rounds, d);
+        probe<<<sms, 128, smem>>>(m, n, chains, il, rounds, d);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
           printf("error %s\n", cudaGetErrorString(e));
@@ -91,9 +92,9 @@ int main(int argc, char** argv) {
         for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
         const double per = static_cast<double>(mx) / (rounds * 4.0 * chains);
         const double floor = 128.0 * n / 256.0;
-        printf("{\"sms\": %d, \"N\": %d, \"chains\": %d, \"interleave\": %d, \"cyc_per_mma\": %.1f, \"floor\": %.0f, "
+        printf("{\"M\": %d, \"sms\": %d, \"N\": %d, \"chains\": %d, \"interleave\": %d, \"cyc_per_mma\": %.1f, \"floor\": %.0f, "
                "\"weight_B_per_cyc\": %.1f}\n",
-               sms, n, chains, il, per, floor, 4096.0 / per);
+               m, sms, n, chains, il, per, floor, 4096.0 / per);
       }
   return 0;
 }
