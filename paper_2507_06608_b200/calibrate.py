@@ -72,6 +72,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--ref-model", default="8b", help="reference ModelConfig preset for the cost model")
+    ap.add_argument("--ref-dims", default=None,
+                    help="hidden,ffn,layers,heads,elem_bytes for ModelConfig::derive when the reference has no "
+                         "preset (e.g. 8192,28672,80,64,2 for Llama-3.1-70B)")
     ap.add_argument("--out", default="profiles/b200_llama3_8b")
     ap.add_argument("--decode-batch", type=int, default=64)
     ap.add_argument("--decode-ctx", type=int, default=600)
@@ -121,7 +124,7 @@ def main():
                            "decode_colocated_ms": statistics.median(co),
                            "slowdown": statistics.median(co) / alone})
 
-    m = nx.model_preset(args.ref_model)
+    m = nx.derive(*[int(v) for v in args.ref_dims.split(",")]) if args.ref_dims else nx.model_preset(args.ref_model)
     pf = fit_prefill(m, [(n, n) for n in pref], [x["sms"] / total for x in sweep["prefill"]],
                      [x["ms"] for x in sweep["prefill"]])
     df = fit_decode(m, [ctx] * B, [x["sms"] / total for x in sweep["decode"]], [x["ms"] for x in sweep["decode"]])
