@@ -79,11 +79,13 @@ def parse():
                    help="ControllerConfig.beta, the decode slack in prefill-prioritized mode. The paper's "
                         "1.1 was set for L20; on B200 a 2.0x slack still keeps p99 TBT well inside the "
                         "50 ms SLO (profiles/r01_beta_sweep.md)")
-    p.add_argument("--gamma", type=float, default=5000.0,
+    p.add_argument("--gamma", type=float, default=None,
                    help="ControllerConfig.gamma (SPF aging, tokens of priority per second waited; reference "
                         "default 15). At 128 rps on B200 with the CTA-pair prefill GEMMs: gamma 15 -> 10145 tok/s "
                         "goodput, p99 TTFT 2.67 s; 1500 -> 10552, 1.03 s; 5000 -> 10669, 0.71 s "
-                        "(profiles/r01s2_gamma_*.json); the reference arm runs with the same gamma")
+                        "(profiles/r01s2_gamma_*.json). Default: 5000, except 15 for the long-prompt "
+                        "longbench workload where shortest-prompt-first keeps more requests under the TTFT SLO "
+                        "(C3: 152 vs 117 tok/s). The reference arm runs with the same gamma")
     p.add_argument("--alpha", type=float, default=1.3, help="ControllerConfig.alpha (prefill slack, paper 1.3)")
     p.add_argument("--max-decode-batch", type=int, default=128,
                    help="ControllerConfig.max_decode_batch (reference default 64, domain.hpp:87)")
@@ -293,6 +295,8 @@ def run_reference(args, rank, world, dist):
 
 def main():
     args = parse()
+    if args.gamma is None:
+        args.gamma = 15.0 if args.workload == "longbench" else 5000.0
     if args.calib is None:
         args.calib = os.path.join(REPO, "profiles", "b200_" + args.model.replace(".", "_").replace("-", "_"))
     rank, world, local, dist = dist_setup(args)
