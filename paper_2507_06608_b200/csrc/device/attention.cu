@@ -361,8 +361,14 @@ __global__ void __launch_bounds__(kThreadsAttn)
 // The tile math is transposed (keys / head dims on the MMA's M side, the
 // G <= 8 query heads of the kv head on its N = 8 side; see the kernel).
 constexpr int kKTD = 32;      // keys per decode tile (two 16-token pages)
-constexpr int kStD = 3;       // ring stages per pair
-constexpr int kPairsD = 4;    // warp pairs per CTA (one CTA per SM)
+#ifndef NX_DEC_STAGES
+#define NX_DEC_STAGES 1
+#endif
+#ifndef NX_DEC_PAIRS
+#define NX_DEC_PAIRS 8
+#endif
+constexpr int kStD = NX_DEC_STAGES;   // ring stages per pair
+constexpr int kPairsD = NX_DEC_PAIRS; // warp pairs per CTA (one CTA per SM)
 constexpr int kWarpsD = 2 * kPairsD;
 constexpr int kTileD = kKTD * kHD;  // elements per K (or V) tile
 
