@@ -349,12 +349,14 @@ __global__ void __launch_bounds__(kThreadsAttn)
 // head. Unit w (a warp pair) of the persistent grid owns the contiguous tile
 // range [w T / W, (w + 1) T / W) (T tiles, W units), so every unit streams
 // the same number of KV bytes regardless of the length mix: no wave
-// quantization, no idle tails. Each pair runs its own 3-stage cp.async.bulk
-// ring (one lane issues 2 pages x K/V = 4 x 4 KB copies per tile),
-// continuing across item boundaries so the pipeline never drains; warp h of
-// the pair takes keys [16 h, 16 h + 16) of every tile (two warps per SMSP
-// in the smem of one ring: the kernel is issue-latency bound, ncu 4.4
-// cycles / instruction with one warp per SMSP), and the pair merges its
+// quantization, no idle tails. Each pair runs its own cp.async.bulk ring of
+// NX_DEC_STAGES stages (one lane issues 2 pages x one 8 KB K|V block per
+// tile), continuing across item boundaries; warp h of the pair takes keys
+// [16 h, 16 h + 16) of every tile. The kernel is issue-latency bound (ncu
+// 4.4 cycles / instruction with one warp per SMSP), so warps beat ring
+// depth: 8 pairs x 1 stage (4 warps per SMSP) streams ~21% more per SM
+// than 4 pairs x 3 stages on a 32-SM lane
+// (profiles/r01s2_attn_decode_bw.md). The pair merges its
 // (m, l, O) at the end of each item segment. An item covered by one unit is
 // finalized in place; an item split across units leaves (m, l, O) partials
 // that decode_combine_kernel folds with a log-sum-exp rescale.
