@@ -178,6 +178,40 @@ nx_model_config nxref_model_derive(int64_t d, int64_t dff, int32_t L, int32_t H,
   return o;
 }
 
+// Reference default-constructed ControllerConfig / KernelProfile / EngineConfig
+// (domain.hpp:45-89, simulator.hpp:36-45), so a caller can build a SimConfig
+// without the product library.
+void nxref_defaults(nx_controller_config* c, nx_kernel_profile* p, nx_engine_config* e) {
+  const ControllerConfig rc{};
+  std::memset(c, 0, sizeof(*c));
+  c->alpha = rc.alpha;
+  c->beta = rc.beta;
+  c->kv_switch_fraction = rc.kv_switch_fraction;
+  c->delta_pp = rc.delta_pp;
+  c->gamma = rc.gamma;
+  c->chunk_size = rc.chunk_size;
+  c->max_decode_batch = rc.max_decode_batch;
+  c->token_budget = rc.token_budget;
+  const KernelProfile rp{};
+  auto put = [](nx_saturation_curve& d, const SaturationCurve& s) {
+    d.r_sat = s.r_sat;
+    d.lambda = s.lambda;
+  };
+  put(p->qkv_proj, rp.qkv_proj);
+  put(p->attn_prefill, rp.attn_prefill);
+  put(p->attn_decode, rp.attn_decode);
+  put(p->attn_out_proj, rp.attn_out_proj);
+  put(p->ffn, rp.ffn);
+  const EngineConfig re{};
+  std::memset(e, 0, sizeof(*e));
+  e->kind = NX_ENGINE_NEXUS;
+  e->static_r_p = re.static_r_p;
+  e->prefill_policy = re.prefill_policy == PrefillPolicy::Fcfs ? NX_PREFILL_FCFS : NX_PREFILL_SPF;
+  e->clock_mode = NX_CLOCK_VIRTUAL;
+  e->timeout_sim_s = re.timeout_sim_s;
+  e->max_events = re.max_events;
+}
+
 int nxref_model_preset(const char* name, nx_model_config* out) {
   auto m = model_preset(name);
   if (!m) return NX_EINVAL;

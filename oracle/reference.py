@@ -48,6 +48,7 @@ def lib() -> C.CDLL:
             "nxref_last_error": (C.c_char_p, []),
             "nxref_free": (None, [C.c_void_p]),
             "nxref_model_derive": (_abi.ModelConfig, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32]),
+            "nxref_defaults": (None, [P(_abi.ControllerConfig), P(_abi.KernelProfile), P(_abi.EngineConfig)]),
             "nxref_model_preset": (C.c_int, [C.c_char_p, P(_abi.ModelConfig)]),
             "nxref_gpu_preset": (C.c_int, [C.c_char_p, P(_abi.GpuSpec)]),
             "nxref_validate_config": (C.c_int, [P(_abi.ModelConfig), P(_abi.GpuSpec), P(_abi.ControllerConfig),
@@ -141,6 +142,49 @@ def model_preset(name: str) -> _abi.ModelConfig:
     m = _abi.ModelConfig()
     _check(lib().nxref_model_preset(name.encode(), C.byref(m)))
     return m
+
+
+def model_derive(hidden_dim: int, ffn_dim: int, num_layers: int, num_heads: int,
+                 element_bytes: int = 2) -> _abi.ModelConfig:
+    """ModelConfig::derive (domain.cpp:7-24) computed by the reference itself."""
+    return lib().nxref_model_derive(hidden_dim, ffn_dim, num_layers, num_heads, element_bytes)
+
+
+def defaults() -> tuple[_abi.ControllerConfig, _abi.KernelProfile, _abi.EngineConfig]:
+    """Default-constructed ControllerConfig / KernelProfile / EngineConfig of the reference."""
+    c, p, e = _abi.ControllerConfig(), _abi.KernelProfile(), _abi.EngineConfig()
+    lib().nxref_defaults(C.byref(c), C.byref(p), C.byref(e))
+    return c, p, e
+
+
+def load_kernel_profile_text(text: str) -> tuple[_abi.KernelProfile, list[str]]:
+    """load_kernel_profile (presets.cpp:128-170) through the reference loader."""
+    p, w = _abi.KernelProfile(), C.c_void_p()
+    rc = lib().nxref_kernel_profile_load_text(text.encode(), C.byref(p), C.byref(w))
+    if rc != 0:
+        raise RuntimeError(lib().nxref_last_error().decode())
+    return p, [x for x in _take(w).splitlines() if x]
+
+
+def kernel_profile_text(p: _abi.KernelProfile) -> str:
+    """kernel_profile_text (presets.cpp:109-126) of the reference."""
+    out = C.c_void_p()
+    _check(lib().nxref_kernel_profile_text(C.byref(p), C.byref(out)))
+    return _take(out)
+
+
+def sim_config(model: _abi.ModelConfig, gpu: _abi.GpuSpec, *, kind: int = _abi.NX_ENGINE_NEXUS,
+               static_r_p: int = 50, ctrl: _abi.ControllerConfig | None = None,
+               profile: _abi.KernelProfile | None = None) -> _abi.SimConfig:
+    """A SimConfig built from reference defaults only (no product library involved)."""
+    c, p, e = defaults()
+    cfg = _abi.SimConfig()
+    cfg.model, cfg.gpu = model, gpu
+    cfg.ctrl = ctrl if ctrl is not None else c
+    cfg.profile = profile if profile is not None else p
+    e.kind, e.static_r_p = kind, static_r_p
+    cfg.engine = e
+    return cfg
 
 
 def gpu_preset(name: str) -> _abi.GpuSpec:

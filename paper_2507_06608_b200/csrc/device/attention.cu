@@ -373,6 +373,13 @@ constexpr int kStD = NX_DEC_STAGES;   // ring stages per pair
 constexpr int kPairsD = NX_DEC_PAIRS; // warp pairs per CTA (one CTA per SM)
 constexpr int kWarpsD = 2 * kPairsD;
 constexpr int kTileD = kKTD * kHD;  // elements per K (or V) tile
+// named barrier 1 + pair must stay below the 16 hardware barriers; the ring,
+// the fp32 staging and the barriers must fit one SM's 227 KB opt-in
+static_assert(kPairsD >= 1 && kPairsD <= 15, "NX_DEC_PAIRS must be in [1, 15]");
+static_assert(kStD >= 1, "NX_DEC_STAGES must be >= 1");
+static_assert(static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 2 * 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
+                      kPairsD * 32 * 4 + 64 <= 227u * 1024u,
+              "NX_DEC_PAIRS x NX_DEC_STAGES exceeds 227 KB of shared memory");
 
 
 // Item (sequence, kv head) holding flattened tile index gt: seq_prefix[s] is
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
                        const __nv_bfloat16* __restrict__ kplane,
                        const __nv_bfloat16* __restrict__ vplane, const AttnSeq* __restrict__ seqs,
                        const int* __restrict__ seq_prefix, int n_seq, long long total, long long W,
-                       const int32_t* __restrict__ pages, int max_pieces,
+                       const int32_t* __restrict__ pages,
                        __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
                        float* __restrict__ part_ml) {
   extern __shared__ __align__(1024) uint8_t smem_attn[];
@@ -654,9 +661,10 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
             *reinterpret_cast<uint4*>(dst + c * 8) = w;
           }
         } else {
-          // piece index of this unit within the item (stream-K ownership rule)
-          const long long first = ((cur.item_start + 1) * W - 1) / total;
-          const size_t slot = (static_cast<size_t>(cur.seq) * hkv + cur.kvh) * max_pieces + (gw - first);
+          // compact partial slot: item + unit. The units of item k are
+          // [first_k, last_k] with first_{k+1} >= last_k, so item + unit is unique
+          // per (item, unit) and below n_items + W (the combine reads item + first + q)
+          const size_t slot = static_cast<size_t>(cur.seq) * hkv + cur.kvh + static_cast<size_t>(gw);
           float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
           for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(stage_a + c * 4);
           if (lane < 4) {
@@ -682,7 +690,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 // head), thread = head dim; items covered by a single warp are skipped.
 __global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ seqs,
                                       const int* __restrict__ seq_prefix, long long total, long long W,
-                                      int max_pieces, const float* __restrict__ part_o,
+                                      const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml, __nv_bfloat16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
@@ -695,7 +703,7 @@ __global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ se
   const long long last = ((s0 + n_tiles) * W - 1) / total;
   const int pieces = static_cast<int>(last - first + 1);
   if (pieces <= 1) return;
-  const size_t slot0 = static_cast<size_t>(item) * max_pieces * g.group + r;
+  const size_t slot0 = (static_cast<size_t>(item) + static_cast<size_t>(first)) * g.group + r;
   float M = -INFINITY;
   for (int q = 0; q < pieces; ++q) M = fmaxf(M, part_ml[(slot0 + static_cast<size_t>(q) * g.group) * 2]);
   float acc = 0.f, L = 0.f;
@@ -728,7 +736,7 @@ __global__ void __launch_bounds__(8 * 32, 1)
     decode_attn_pages_kernel(AttnGeom g, const __nv_bfloat16* __restrict__ qkv,
                              const __nv_bfloat16* __restrict__ kvbase, const AttnSeq* __restrict__ seqs,
                              const int* __restrict__ seq_prefix, int n_seq, long long total, long long W,
-                             const int32_t* __restrict__ pages, int max_pieces, __nv_bfloat16* __restrict__ out,
+                             const int32_t* __restrict__ pages, __nv_bfloat16* __restrict__ out,
                              float* __restrict__ part_o, float* __restrict__ part_ml) {
   extern __shared__ __align__(1024) uint8_t smem_attn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -906,8 +914,8 @@ __global__ void __launch_bounds__(8 * 32, 1)
           *reinterpret_cast<uint4*>(dst + c * 8) = w;
         }
       } else {
-        const long long first = ((static_cast<long long>(seq_prefix[seq]) + 1) * W - 1) / total;
-        const size_t slot = (static_cast<size_t>(seq) * hkv + warp) * max_pieces + static_cast<size_t>(u - first);
+        // compact slot (sequence + unit) x kv head, unique as in the pair kernel
+        const size_t slot = (static_cast<size_t>(seq) + static_cast<size_t>(u)) * hkv + warp;
         float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
         for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(wstage + c * 4);
         if (lane < 4) {
@@ -930,7 +938,7 @@ __global__ void __launch_bounds__(8 * 32, 1)
 // decode): CTA = (sequence, kv head, query head), thread = head dim.
 __global__ void decode_combine_pages_kernel(AttnGeom g, const AttnSeq* __restrict__ seqs,
                                             const int* __restrict__ seq_prefix, long long total, long long W,
-                                            int max_pieces, const float* __restrict__ part_o,
+                                            const float* __restrict__ part_o,
                                             const float* __restrict__ part_ml, __nv_bfloat16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
@@ -942,12 +950,12 @@ __global__ void decode_combine_pages_kernel(AttnGeom g, const AttnSeq* __restric
   const long long last = (t1 * W - 1) / total;
   const int pieces = static_cast<int>(last - first + 1);
   if (pieces <= 1) return;
-  const size_t slot0 = static_cast<size_t>(item) * max_pieces * g.group + r;
+  const size_t slot0 = ((static_cast<size_t>(seq) + static_cast<size_t>(first)) * hkv + kvh) * g.group + r;
   float M = -INFINITY;
-  for (int q = 0; q < pieces; ++q) M = fmaxf(M, part_ml[(slot0 + static_cast<size_t>(q) * g.group) * 2]);
+  for (int q = 0; q < pieces; ++q) M = fmaxf(M, part_ml[(slot0 + static_cast<size_t>(q) * hkv * g.group) * 2]);
   float acc = 0.f, L = 0.f;
   for (int q = 0; q < pieces; ++q) {
-    const size_t slot = slot0 + static_cast<size_t>(q) * g.group;
+    const size_t slot = slot0 + static_cast<size_t>(q) * hkv * g.group;
     const float ms = part_ml[slot * 2];
     const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
     L += part_ml[slot * 2 + 1] * w;
@@ -976,7 +984,7 @@ cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                               const AttnSeq* seqs, const int2* work, int n_work,
                               const int32_t* pages, __nv_bfloat16* out, cudaStream_t s) {
   if (n_work == 0) return cudaSuccess;
-  ensure_kernels_prepared();
+  if (const cudaError_t pe = ensure_kernels_prepared(); pe != cudaSuccess) return pe;
   const size_t smem = attn_smem_bytes_pf();
   ++g_kernel_launches;
   return launch_pdl(prefill_attn_kernel, dim3(n_work, g.n_kv_heads), dim3(kThreadsAttn), smem, s, g, qkv,
@@ -991,7 +999,7 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              int sm_count, cudaStream_t s) {
   if (n_seq == 0 || total_tiles == 0) return cudaSuccess;
   if (g.group > 8) return cudaErrorInvalidValue;
-  ensure_kernels_prepared();
+  if (const cudaError_t pe = ensure_kernels_prepared(); pe != cudaSuccess) return pe;
   // NX_DEC_ATTN=pages: the page-major variant (64 KB copies; measured ~4%
   // slower than the warp-pair kernel on 48 SMs: both are issue-bound)
   static const bool pages_major = [] {
@@ -1001,48 +1009,48 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (pages_major && g.n_kv_heads <= 8) {
     const long long T = total_tiles / g.n_kv_heads;  // 32-key tiles, sequence-major
     const long long W = std::min<long long>(sm_count, T);
-    const long long per_min = std::max<long long>(1, T / W);
-    const int max_pieces = static_cast<int>((max_seq_tiles + per_min - 1) / per_min) + 1;
-    if (static_cast<size_t>(n_seq) * g.n_kv_heads * max_pieces * g.group * kHD > part_cap)
-      return cudaErrorInvalidValue;
+    // compact slots: (sequence + unit) x kv head < (n_seq + W) x Hkv
+    if (static_cast<size_t>(n_seq + W) * g.n_kv_heads * g.group * kHD > part_cap) return cudaErrorInvalidValue;
     const size_t smem = attn_smem_bytes_dec_pages(g.n_kv_heads);
     ++g_kernel_launches;
     cudaError_t e = launch_pdl(decode_attn_pages_kernel, dim3(static_cast<unsigned>(W)), dim3(g.n_kv_heads * 32),
-                               smem, s, g, qkv, kplane, seqs, seq_prefix, n_seq, T, W, pages, max_pieces, out,
+                               smem, s, g, qkv, kplane, seqs, seq_prefix, n_seq, T, W, pages, out,
                                part_o, part_ml);
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
     return launch_pdl(decode_combine_pages_kernel, dim3(n_seq * g.n_kv_heads, g.group), dim3(kHD), 0, s, g, seqs,
-                      seq_prefix, T, W, max_pieces, part_o, part_ml, out);
+                      seq_prefix, T, W, part_o, part_ml, out);
   }
   const size_t smem = attn_smem_bytes_dec();
   const long long W = std::min<long long>(static_cast<long long>(sm_count) * kPairsD, total_tiles);
   const int grid = static_cast<int>((W + kPairsD - 1) / kPairsD);
-  // pieces per item <= ceil(tiles / min range) + 1
-  const long long per_min = std::max<long long>(1, total_tiles / W);
-  const int max_pieces = static_cast<int>((max_seq_tiles + per_min - 1) / per_min) + 1;
-  if (static_cast<size_t>(n_seq) * g.n_kv_heads * max_pieces * g.group * kHD > part_cap)
+  // compact partial slots: item + unit < n_seq * Hkv + W, independent of how
+  // many pieces the longest item splits into
+  if ((static_cast<size_t>(n_seq) * g.n_kv_heads + static_cast<size_t>(W)) * g.group * kHD > part_cap)
     return cudaErrorInvalidValue;
   ++g_kernel_launches;
   cudaError_t e = launch_pdl(decode_attn_kernel, dim3(grid), dim3(kWarpsD * 32), smem, s, g, qkv, kplane,
-                             vplane, seqs, seq_prefix, n_seq, total_tiles, W, pages, max_pieces, out,
+                             vplane, seqs, seq_prefix, n_seq, total_tiles, W, pages, out,
                              part_o, part_ml);
   if (e != cudaSuccess) return e;
   ++g_kernel_launches;
   return launch_pdl(decode_combine_kernel, dim3(n_seq * g.n_kv_heads, g.group), dim3(kHD), 0, s, g, seqs,
-                    seq_prefix, total_tiles, W, max_pieces, part_o, part_ml, out);
+                    seq_prefix, total_tiles, W, part_o, part_ml, out);
 }
 
-void prepare_attention_kernels() {
-  cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(attn_smem_bytes_pf()));
-  cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(attn_smem_bytes_dec()));
-  cudaFuncSetAttribute(decode_attn_pages_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(attn_smem_bytes_dec_pages(8)));
+cudaError_t prepare_attention_kernels() {
+  cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(attn_smem_bytes_pf()));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(attn_smem_bytes_dec()));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(decode_attn_pages_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(attn_smem_bytes_dec_pages(8)));
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, decode_combine_pages_kernel);
-  cudaFuncGetAttributes(&fa, decode_combine_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, decode_combine_pages_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, decode_combine_kernel);
+  return e;
 }
 
 }  // namespace nxd

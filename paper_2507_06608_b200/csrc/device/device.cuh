@@ -42,9 +42,9 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 // Load every kernel and set its shared-memory opt-in on the current device
 // (once per device; see kernels.cu).
-void ensure_kernels_prepared();
+cudaError_t ensure_kernels_prepared();
 void prepare_gemm_kernels();
-void prepare_attention_kernels();
+cudaError_t prepare_attention_kernels();
 void prepare_tp_kernels();
 
 // ---- GEMM (gemm_tc.cu) -------------------------------------------------------

@@ -555,19 +555,22 @@ bool g_pdl = [] {
   return !(e && e[0] == '0');
 }();
 
-void ensure_kernels_prepared() {
+cudaError_t ensure_kernels_prepared() {
   static std::atomic<uint64_t> mask{0};
+  static cudaError_t failed[64] = {};
   int d = 0;
   cudaGetDevice(&d);
   const uint64_t bit = 1ull << (d & 63);
-  if (mask.load(std::memory_order_acquire) & bit) return;
+  if (mask.load(std::memory_order_acquire) & bit) return failed[d & 63];
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
-  if (mask.load() & bit) return;
+  if (mask.load() & bit) return failed[d & 63];
   prepare_gemm_kernels();
   prepare_gemm_decode_kernel();
   prepare_gemm_pair_kernel();
-  prepare_attention_kernels();
+  // a rejected smem opt-in would make every launch of that kernel fail later
+  // with no clear cause: remember it and hand it to the launch wrappers
+  failed[d & 63] = prepare_attention_kernels();
   prepare_tp_kernels();
   const void* fns[] = {reinterpret_cast<const void*>(fill_random_kernel),
                        reinterpret_cast<const void*>(fill_random_slice_kernel),
@@ -586,6 +589,7 @@ void ensure_kernels_prepared() {
   for (const void* f : fns) cudaFuncGetAttributes(&fa, f);
   cudaGetLastError();
   mask.fetch_or(bit);
+  return failed[d & 63];
 }
 
 }  // namespace nxd
