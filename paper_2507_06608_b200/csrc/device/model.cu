@@ -479,6 +479,14 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   ws.prof = sample_every_ > 0 && (ws.batch_counter++ % static_cast<uint64_t>(sample_every_)) == 0;
   ws.recs.clear();
   ws.ev_used = 0;
+  // Two lanes never share SMs: when this batch or the other lane's batch still
+  // in flight runs on the whole GPU (a decode batch while the prefill lane is
+  // idle, Engine::dispatch_device), this one is ordered after it.
+  if (parts_.enabled && slot < 2) {
+    const LaneWs& other = lanes_[1 - slot];
+    if (other.pending && (other.layout < 0 || ws.layout < 0))
+      ck(cudaStreamWaitEvent(s, other.ev_end, 0), "lane order");
+  }
   ck(cudaEventRecord(ws.ev_start, s), "event record");
   ck(cudaMemcpyAsync(ws.meta_dev, hp, off, cudaMemcpyHostToDevice, s), "meta h2d");
   const uint8_t* dp = ws.meta_dev;

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <thread>
 
@@ -55,6 +56,7 @@ Engine::Engine(const nx_sim_config& cfg)
     if (r < 1 || r > 99) throw InvalidArg("static partition share must lie in [1, 99]");
     ctl_ = Controller(nx_partition_state{r, 100 - r, r}, cfg.ctrl);
   }
+  if (const char* e = std::getenv("NX_DECODE_FULL_IDLE")) decode_full_when_idle_ = std::atoi(e) != 0;
   if (cfg.engine.clock_mode < NX_CLOCK_VIRTUAL || cfg.engine.clock_mode > NX_CLOCK_REPLAY)
     throw InvalidArg("unknown clock mode");
   // Default page pool: enough pages for the whole byte capacity plus one
@@ -278,6 +280,13 @@ void Engine::dispatch_device(Lane& lane, int slot, int lane_kind) {
   b.sm_pct = lane_kind == NX_LANE_MIXED ? 100
              : lane_kind == NX_LANE_PREFILL ? lane.r_p
                                             : 100 - lane.r_p;
+  // Device layout only (the decision log keeps the controller's r_p): a
+  // decode batch launched while the prefill lane is idle and no prompt waits
+  // runs on the whole GPU instead of leaving the prefill SMs dark. A prefill
+  // batch launched before it finishes is ordered after it by the executor
+  // (Model::launch), so the two never share SMs.
+  if (lane_kind == NX_LANE_DECODE && decode_full_when_idle_ && !prefill_.busy && prefill_queue().empty())
+    b.sm_pct = 100;
   for (const auto& m : lane.dec) {
     const Live& l = live(m.id);
     const std::vector<int32_t>* pt = pages_.table(m.id);

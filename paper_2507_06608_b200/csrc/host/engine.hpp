@@ -132,6 +132,7 @@ class Engine {
 
   nx_sim_config cfg_;
   bool dynamic_, monolithic_;
+  bool decode_full_when_idle_ = true;  // NX_DECODE_FULL_IDLE=0 disables (A/B)
   Controller ctl_;
   std::vector<Live> reqs_;
   std::unordered_map<uint64_t, size_t> index_;

@@ -84,6 +84,13 @@ def _prefer_torch_nccl():
 
 _prefer_torch_nccl()
 
+# Each lane of each rank is its own stream; with the default 8 hardware
+# work queues, 16+ streams (TP=8 colocated: 8 ranks x 2 lanes) alias queues,
+# and a rank's spinning peer all-reduce can then sit in front of the very
+# kernel it waits for. Read by the driver at context creation (C++ hosts that
+# drive colocated TP groups set it themselves).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 
 def shard_plan(a: Arch, tp_size: int, rank: int) -> TpShard:
     """nx_tp_shard_plan: the heads / ffn features / vocab rows rank owns."""

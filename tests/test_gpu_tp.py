@@ -27,10 +27,12 @@ def D():
 ARCHES = {
     2: dict(hidden=512, n_layers=2, n_heads=8, n_kv_heads=2, ffn=1536, vocab=2048, rope_theta=10000.0),
     4: dict(hidden=512, n_layers=2, n_heads=8, n_kv_heads=4, ffn=1024, vocab=1920, rope_theta=10000.0),
+    # 8 kv heads, one per rank (the Llama-3.1-70B split at TP=8: 8 q + 1 kv head per GPU)
+    8: dict(hidden=2048, n_layers=2, n_heads=16, n_kv_heads=8, ffn=2048, vocab=3072, rope_theta=500000.0),
 }
 
 
-@pytest.fixture(scope="module", params=[2, 4])
+@pytest.fixture(scope="module", params=[2, 4, 8])
 def pair(request, D):
     from oracle.llama_fp32 import LlamaFP32
     tp = request.param
