@@ -176,6 +176,17 @@ struct AttnGeom {
   float scale_log2;
 };
 
+// Paged KV cache, per layer [page][kv head][K | V] blocks of 16 token rows
+// x 128 dims (8 KB). Each K (V) half is 4 KB = four 1 KB SWIZZLE_128B atoms:
+// atom (r / 8, c / 8) -- 8 token rows x 64 dims -- sits at (2 (r / 8) + c / 8)
+// KB, and 16 B chunk c of token row r at kv_chunk_elem(r, c) (elements).
+// The K (V) halves of consecutive pages copied 4 KB apart into shared memory
+// form one uniform UMMA operand (8-token atoms 2 KB apart, 64-dim halves
+// 1 KB apart): K-major for S = Q K^T, MN-major for O = P V.
+__host__ __device__ __forceinline__ int kv_chunk_elem(int r, int c) {
+  return ((((r >> 3) << 1) | (c >> 3)) << 9) + ((r & 7) << 6) + ((((c & 7) ^ (r & 7))) << 3);
+}
+
 struct AttnSeq {
   int q_start;   // first row of this sequence in the batch
   int q_len;     // new tokens this launch
@@ -183,12 +194,17 @@ struct AttnSeq {
   int page_off;  // offset of the sequence's page list in the batch page array
 };
 
-size_t attn_smem_bytes();
-// work[i] = {sequence index, first query row} of 64-row blocks.
-cudaError_t prefill_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
-                              const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
-                              const AttnSeq* seqs, const int2* work, int n_work,
-                              const int32_t* pages, __nv_bfloat16* out, cudaStream_t s);
+// Prefill attention (attn_prefill.cu, tcgen05): work[i] = {sequence index,
+// first token} of items of prefill_attn_tokens_per_item(group) tokens (x G
+// heads = up to 128 query rows), longest first; qmap = encode_q_heads_map over
+// the lane's qkv buffer; kvplane = the layer's [page][kv head][K | V] blocks.
+int prefill_attn_tokens_per_item(int group);
+bool encode_q_heads_map(CUtensorMap* map, const void* qkv, int tokens, int n_heads, int group,
+                        int row_stride_elems);
+cudaError_t prefill_attention(const AttnGeom& g, const CUtensorMap& qmap, const __nv_bfloat16* kvplane,
+                              const AttnSeq* seqs, const int2* work, int n_work, const int32_t* pages,
+                              __nv_bfloat16* out, int sm_count, cudaStream_t s);
+cudaError_t prepare_prefill_attention_kernel();
 // Decode attention over 32-key tiles (kDecTileKeys): seq_prefix[s] = first
 // tile of sequence s, sum_{s' < s} ceil(kv_len(s') / 32) (n_seq + 1 entries,
 // device memory); total_tiles = seq_prefix[n_seq] * n_kv_heads.

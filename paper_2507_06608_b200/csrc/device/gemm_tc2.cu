@@ -289,11 +289,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                   *reinterpret_cast<uint4*>(dst + grp * 8) = *reinterpret_cast<uint4*>(ra);
                   *reinterpret_cast<uint4*>(dst + 64 + grp * 8) = *reinterpret_cast<uint4*>(rb);
                 } else {
-                  const int sl = rk.slot[t], page = sl / rk.page_tokens, off = sl % rk.page_tokens, sw = off & 7;
+                  const int sl = rk.slot[t], page = sl / rk.page_tokens, off = sl % rk.page_tokens;
                   __nv_bfloat16* dst =
-                      rk.kplane + ((static_cast<size_t>(page) * nkv + (head - nq)) * 2 * rk.page_tokens + off) * kBM;
-                  *reinterpret_cast<uint4*>(dst + ((grp ^ sw) << 3)) = *reinterpret_cast<uint4*>(ra);
-                  *reinterpret_cast<uint4*>(dst + (((grp + 8) ^ sw) << 3)) = *reinterpret_cast<uint4*>(rb);
+                      rk.kplane + (static_cast<size_t>(page) * nkv + (head - nq)) * 2 * rk.page_tokens * kBM;
+                  *reinterpret_cast<uint4*>(dst + kv_chunk_elem(off, grp)) = *reinterpret_cast<uint4*>(ra);
+                  *reinterpret_cast<uint4*>(dst + kv_chunk_elem(off, grp + 8)) = *reinterpret_cast<uint4*>(rb);
                 }
               }
             }
@@ -309,8 +309,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16(rnd(j, c * 8 + i));
                 const int sl = rk.slot[t], page = sl / rk.page_tokens, off = sl % rk.page_tokens;
                 __nv_bfloat16* dst =
-                    rk.vplane + ((static_cast<size_t>(page) * nkv + (head - nq - nkv)) * 2 * rk.page_tokens + off) * kBM;
-                *reinterpret_cast<uint4*>(dst + ((c ^ (off & 7)) << 3)) = *reinterpret_cast<uint4*>(o);
+                    rk.vplane + (static_cast<size_t>(page) * nkv + (head - nq - nkv)) * 2 * rk.page_tokens * kBM;
+                *reinterpret_cast<uint4*>(dst + kv_chunk_elem(off, c)) = *reinterpret_cast<uint4*>(o);
               }
             }
           }

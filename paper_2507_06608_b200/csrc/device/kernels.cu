@@ -99,15 +99,13 @@ __global__ void rope_table_kernel(const int32_t* __restrict__ pos, const float* 
 // One token's RoPE + paged KV write. Work items: (q or k head, chunk pair p)
 // rotates dims [8p, 8p+8) with [64+8p, 64+8p+8) (rotate-half, hd = 128)
 // using 16 B vectors; q goes to qdst (the qkv row the attention reads), k and
-// v go to the paged cache in the pre-swizzled layout (16 B chunk c of page
-// row r at c ^ (r & 7)). `row` may live in global or shared memory.
+// v go to the paged cache in its UMMA atom layout (kv_chunk_elem, device.cuh). `row` may live in global or shared memory.
 __device__ __forceinline__ void rope_kv_token(const __nv_bfloat16* row, __nv_bfloat16* qdst, int s,
                                               const float2* __restrict__ cs, int n_heads, int n_kv_heads,
                                               int page_tokens, __nv_bfloat16* __restrict__ kplane,
                                               __nv_bfloat16* __restrict__ vplane) {
   constexpr int hd = 128, half = 64;
   const int page = s / page_tokens, off = s % page_tokens;
-  const int sw = off & 7;
   const int rot_items = (n_heads + n_kv_heads) * 8;
   const int v_items = n_kv_heads * 16;
   for (int it = threadIdx.x; it < rot_items + v_items; it += blockDim.x) {
@@ -130,17 +128,17 @@ __device__ __forceinline__ void rope_kv_token(const __nv_bfloat16* row, __nv_bfl
         *reinterpret_cast<uint4*>(qdst + head * hd + 8 * p) = *reinterpret_cast<uint4*>(ra);
         *reinterpret_cast<uint4*>(qdst + head * hd + half + 8 * p) = *reinterpret_cast<uint4*>(rb);
       } else {
-        __nv_bfloat16* dst =  // interleaved [page][kv head][K | V][page_tokens][hd] blocks
-            kplane + ((static_cast<size_t>(page) * n_kv_heads + (head - n_heads)) * 2 * page_tokens + off) * hd;
-        *reinterpret_cast<uint4*>(dst + ((p ^ sw) << 3)) = *reinterpret_cast<uint4*>(ra);
-        *reinterpret_cast<uint4*>(dst + (((p + 8) ^ sw) << 3)) = *reinterpret_cast<uint4*>(rb);
+        __nv_bfloat16* dst =  // [page][kv head][K | V] blocks of 4 KB atoms (kv_chunk_elem)
+            kplane + (static_cast<size_t>(page) * n_kv_heads + (head - n_heads)) * 2 * page_tokens * hd;
+        *reinterpret_cast<uint4*>(dst + kv_chunk_elem(off, p)) = *reinterpret_cast<uint4*>(ra);
+        *reinterpret_cast<uint4*>(dst + kv_chunk_elem(off, p + 8)) = *reinterpret_cast<uint4*>(rb);
       }
     } else {
       const int i = it - rot_items;
       const int kh = i >> 4, c = i & 15;
       const __nv_bfloat16* src = row + (n_heads + n_kv_heads + kh) * hd + c * 8;
-      __nv_bfloat16* dst = vplane + ((static_cast<size_t>(page) * n_kv_heads + kh) * 2 * page_tokens + off) * hd;
-      *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 3)) = *reinterpret_cast<const uint4*>(src);
+      __nv_bfloat16* dst = vplane + (static_cast<size_t>(page) * n_kv_heads + kh) * 2 * page_tokens * hd;
+      *reinterpret_cast<uint4*>(dst + kv_chunk_elem(off, c)) = *reinterpret_cast<const uint4*>(src);
     }
   }
 }

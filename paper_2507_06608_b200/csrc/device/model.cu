@@ -370,6 +370,8 @@ void LaneWs::init(Model* m, int max_tokens) {
         !encode_kmajor(&map_hs[i], hs, sample_cap, a.hidden, static_cast<size_t>(a.hidden) * 2, bn))
       throw std::runtime_error("cuTensorMapEncodeTiled failed (activations)");
   }
+  if (!encode_q_heads_map(&map_q, qkv, T, m->hq_, m->hq_ / m->hkv_, m->qkv_rows_))
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (prefill attention q)");
 }
 
 void LaneWs::release() {
@@ -417,9 +419,10 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   const size_t o_pages = carve(n_pages_total * 4 + 4);
   const size_t o_rows = carve(n_sample * 4 + 4);
   const size_t o_dpre = carve((n_seq + 1) * 4);
+  const int tq = prefill_attn_tokens_per_item(hq_ / hkv_);
   int max_work = 0;
   for (const auto& m : b.members)
-    max_work += (m.n_tokens * (hq_ / hkv_) + 63) / 64;
+    max_work += (m.n_tokens + tq - 1) / tq;
   const size_t o_work = carve(static_cast<size_t>(max_work) * sizeof(int2) + 8);
   int32_t* tok = reinterpret_cast<int32_t*>(hp + o_tok);
   int32_t* pos = reinterpret_cast<int32_t*>(hp + o_pos);
@@ -429,7 +432,6 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
   int32_t* rows = reinterpret_cast<int32_t*>(hp + o_rows);
   int2* work = reinterpret_cast<int2*>(hp + o_work);
   int32_t* dpre = reinterpret_cast<int32_t*>(hp + o_dpre);
-  const int group = hq_ / hkv_;
   int t = 0, pg = 0, ns = 0, nw = 0;
   ws.dec_seq_count = 0;
   ws.max_dec_kv = 0;
@@ -466,11 +468,17 @@ void Model::launch(int slot, const nxb::ExecBatch& b) {
       const double st = static_cast<double>(m.start_pos), q = m.n_tokens;
       ws.pre_kv_tokens += s.kv_len;
       ws.pre_pairs += q * st + q * (q + 1) / 2;
-      for (int r = 0; r < m.n_tokens * group; r += 64) work[nw++] = make_int2(i, r);
+      for (int t0 = 0; t0 < m.n_tokens; t0 += tq) work[nw++] = make_int2(i, t0);
     }
     t += m.n_tokens;
     pg += m.n_pages;
   }
+  // prefill attention items longest first (persistent CTAs take them round robin)
+  auto item_tiles = [&](const int2& w) {
+    const AttnSeq& q = seqs[w.x];
+    return q.kv_len - q.q_len + std::min(q.q_len, w.y + tq);
+  };
+  std::stable_sort(work, work + nw, [&](const int2& a, const int2& c) { return item_tiles(a) > item_tiles(c); });
   ws.tokens = T;
   ws.n_seq = n_seq;
   ws.n_work = nw;
@@ -561,8 +569,9 @@ void Model::forward(LaneWs& ws) {
   auto pbytes = [&](double rows) { return Td * rows * 4; };
   for (int l = 0; l < a_.n_layers; ++l) {
     const LayerW& w = layers_[l];
-    // layer l: [page][kv head][K | V][page_tokens][hd] (one contiguous 8 KB block
-    // per (page, kv head)); the V view starts one K half-block on
+    // layer l: [page][kv head][K | V] blocks of 16 x 128 (one contiguous 8 KB
+    // block per (page, kv head), kv_chunk_elem atoms); the V view starts one K
+    // half-block on
     __nv_bfloat16* kplane = kv_ + (2 * static_cast<size_t>(l)) * plane_elems_;
     __nv_bfloat16* vplane = kplane + static_cast<size_t>(cfg_.page_tokens) * a_.head_dim;
     RopeKV rope;
@@ -610,8 +619,8 @@ void Model::forward(LaneWs& ws) {
     if (ws.n_work > 0)
       timed(NX_K_ATTN_PREFILL, ws.pre_kv_tokens * kvtok + (Td - ws.dec_seq_count) * qo,
             4.0 * ws.pre_pairs * attn_cols_, [&] {
-              ck(prefill_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.d_work, ws.n_work,
-                                   ws.d_pages, ws.attn, s),
+              ck(prefill_attention(g, ws.map_q, kplane, ws.d_seqs, ws.d_work, ws.n_work, ws.d_pages,
+                                   ws.attn, sm, s),
                  "prefill attention");
             });
     // Row-parallel under TP: rank 0 adds the residual, the others store

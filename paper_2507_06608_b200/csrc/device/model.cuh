@@ -64,6 +64,7 @@ struct LaneWs {
   float *part_o = nullptr, *part_ml = nullptr;
   size_t part_cap = 0;
   CUtensorMap map_h[4], map_attn[4], map_act[4], map_hs[4];
+  CUtensorMap map_q;  // q heads of the qkv buffer for prefill attention (encode_q_heads_map)
   uint8_t* meta_dev = nullptr;
   uint8_t* meta_host = nullptr;
   size_t meta_bytes = 0;
