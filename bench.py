@@ -142,7 +142,7 @@ def log_metrics(event_log: str, slo_ttft: float, slo_tbt: float):
                 times.setdefault(rid, []).extend([t] * emitted)
             elif kind == "finish":
                 finish[rid] = t
-    ttft, gaps_all, good, out_tokens = [], [], 0, 0
+    ttft, gaps_all, good, out_tokens, good_reqs = [], [], 0, 0, 0
     for rid, f in finish.items():
         ts = times[rid]
         tt = ts[0] - arrival[rid]
@@ -153,10 +153,11 @@ def log_metrics(event_log: str, slo_ttft: float, slo_tbt: float):
         p99 = sorted(gaps)[max(0, -(-99 * len(gaps) // 100) - 1)] if gaps else 0.0
         if tt <= slo_ttft and p99 <= slo_tbt:
             good += len(ts)
+            good_reqs += 1
     span = (max(finish.values()) - min(arrival.values())) if finish else 0.0
     window = (max(arrival.values()) - min(arrival.values())) if arrival else 0.0
     return dict(good_tokens=good, out_tokens=out_tokens, makespan=span, window=window, ttft=ttft,
-                tbt=gaps_all, completed=len(finish))
+                tbt=gaps_all, completed=len(finish), good_requests=good_reqs)
 
 
 def nearest_rank(v, p):

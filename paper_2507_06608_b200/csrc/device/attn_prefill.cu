@@ -240,7 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 4; ++c) tmem_ld32(trow + kTmemS + b * 128 + 32 * c, v[c]);
         tmem_ld_wait();
         const int k0 = j * kKeys;
-        float mx = -INFINITY;
+        // four independent max chains (one per 32-column chunk): one warp per
+        // SM sub-partition, so ILP is the only latency hiding there is
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (k0 + kKeys - 1 > limit) {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
@@ -248,14 +250,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) {
               const float sv = (k0 + 32 * c + i <= limit) ? __uint_as_float(v[c][i]) : -INFINITY;
               v[c][i] = __float_as_uint(sv);
-              mx = fmaxf(mx, sv);
+              mx4[c] = fmaxf(mx4[c], sv);
             }
         } else {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[c][i]));
+            for (int i = 0; i < 32; ++i) mx4[c] = fmaxf(mx4[c], __uint_as_float(v[c][i]));
         }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
         const float mnew = mx * g.scale_log2;  // -inf stays -inf
         const bool resc = mnew > m + 8.f;
         if (__any_sync(0xffffffffu, resc && j > 0)) {
@@ -279,19 +282,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = mnew;
         }
         const float mb = m == -INFINITY ? 0.f : m;
+        float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t pk[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int e = 64 * c + 2 * i;
-            const float p0 = ex2(fmaf(__uint_as_float(v[e >> 5][e & 31]), g.scale_log2, -mb));
-            const float p1 = ex2(fmaf(__uint_as_float(v[(e + 1) >> 5][(e + 1) & 31]), g.scale_log2, -mb));
-            l += p0 + p1;
+            const float x0 = fmaf(__uint_as_float(v[e >> 5][e & 31]), g.scale_log2, -mb);
+            const float x1 = fmaf(__uint_as_float(v[(e + 1) >> 5][(e + 1) & 31]), g.scale_log2, -mb);
+            const float p0 = ex2(x0), p1 = ex2(x1);
+            ls[i & 7] += p0 + p1;
             pk[i] = pack_bf16(p0, p1);
           }
           tmem_st32(trow + kTmemS + b * 128 + 32 * c, pk);
         }
+        l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[b]);

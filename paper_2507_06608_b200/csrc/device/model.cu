@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <initializer_list>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -41,6 +43,16 @@ void Partitions::init(int device, bool enable) {
   ck(cudaStreamCreateWithFlags(&full_stream, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&plain_stream[0], cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&plain_stream[1], cudaStreamNonBlocking), "stream");
+  // Kernels launched on green-context streams cannot be replayed by Nsight
+  // Compute (the profiled process dies at the first such launch). Under a
+  // profiler's injection library the lanes therefore run on plain streams
+  // (same kernels, no SM partitions) unless NX_GREEN_UNDER_PROFILER=1.
+  const bool profiler = std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
+                        std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") || std::getenv("CUDA_INJECTION64_PATH");
+  if (enable && profiler && !std::getenv("NX_GREEN_UNDER_PROFILER")) {
+    std::fprintf(stderr, "nexus_b200: profiler injection detected, green-context partitions disabled\n");
+    enable = false;
+  }
   if (!enable) return;
   auto sym = [](const char* name) {
     void* p = nullptr;
