@@ -66,8 +66,10 @@ def parse():
     p.add_argument("--workload", default="sharegpt",
                    help="trace preset: sharegpt | mixed | long-data | arxiv | longbench | bursty")
     p.add_argument("--kv-gb", type=float, default=80.0)
-    p.add_argument("--slo-ttft", type=float, default=1.0)
-    p.add_argument("--slo-tbt", type=float, default=0.05)
+    p.add_argument("--slo-ttft", type=float, default=None,
+                   help="TTFT SLO (s); default per model as frozen in BASELINE.md: 8B 1, 14B 4, 70B 2")
+    p.add_argument("--slo-tbt", type=float, default=None,
+                   help="per-request p99 TBT SLO (s); default 8B 0.05, 14B 0.075, 70B 0.1")
     p.add_argument("--profile-every", type=int, default=8)
     p.add_argument("--seed", type=int, default=101,
                    help="trace seed of the first step (seed + step per step). The controller knobs were swept "
@@ -94,6 +96,12 @@ def parse():
                         "longbench workload where shortest-prompt-first keeps more requests under the TTFT SLO "
                         "(C3: 152 vs 117 tok/s). The reference arm runs with the same gamma")
     p.add_argument("--alpha", type=float, default=1.3, help="ControllerConfig.alpha (prefill slack, paper 1.3)")
+    p.add_argument("--tp", type=int, default=0,
+                   help="tensor-parallel group size (C4). 0 = auto: under torchrun with --model llama3-70b the "
+                        "whole job is one TP group of WORLD_SIZE GPUs driven by rank 0 (NX_TP_PEER: our peer-memory "
+                        "all-reduce kernels over NVLink, one engine, device clock); otherwise 1")
+    p.add_argument("--tp-colocated", action="store_true",
+                   help="place all TP ranks on one GPU (NX_TP_PEER_COLOCATED; a functional check of the TP path)")
     p.add_argument("--max-decode-batch", type=int, default=128,
                    help="ControllerConfig.max_decode_batch (reference default 64, domain.hpp:87)")
     return p.parse_args()
@@ -231,13 +239,15 @@ def load_calib(base):
 
 
 def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True, max_decode_batch=64,
-             alpha=1.3, beta=1.1, model="llama3-8b", gamma=None, static_r_p=50):
+             alpha=1.3, beta=1.1, model="llama3-8b", gamma=None, static_r_p=50, tp=1):
+    """tp > 1: the GpuSpec describes the TP group (peaks x tp; every GPU holds
+    its kv heads of the same token pages, so the token capacity is one GPU's)."""
     m = nx.derive(*MODELS[model][0])
     slack = 4096
     cap_tokens = (num_pages - slack) * page_tokens
     cal = load_calib(calib)
     C, B, prof, bw_sat = (1.6595e15, 6.5562e12, None, None) if cal is None else cal
-    g = nx.gpu_spec(148, C, B, cap_tokens * ref_kvbpt(model))
+    g = nx.gpu_spec(148, C * tp, B * tp, cap_tokens * ref_kvbpt(model))
     kind = {"nexus": nx.NX_ENGINE_NEXUS, "static": nx.NX_ENGINE_STATIC,
             "monolithic": nx.NX_ENGINE_MONOLITHIC}[engine]
     ctrl = nx.lib().nx_controller_config_default()
@@ -338,6 +348,9 @@ def run_reference(args, rank, world, dist):
 
 def main():
     args = parse()
+    slo = {"llama3-8b": (1.0, 0.05), "qwen2.5-14b": (4.0, 0.075), "llama3-70b": (2.0, 0.1)}[args.model]
+    args.slo_ttft = slo[0] if args.slo_ttft is None else args.slo_ttft
+    args.slo_tbt = slo[1] if args.slo_tbt is None else args.slo_tbt
     if args.gamma is None:
         args.gamma = 15.0 if args.workload == "longbench" else 5000.0
     if args.calib is None:
@@ -346,20 +359,34 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world, dist)
         return
+    tp = args.tp or (world if args.model == "llama3-70b" and world > 1 else 1)
+    if tp > 1 and world > 1:
+        # one TP group over all GPUs of the job, driven by rank 0 (one engine,
+        # one device clock); the other ranks only hold the barriers
+        if tp != world:
+            raise SystemExit(f"--tp {tp} must equal WORLD_SIZE {world} under torchrun")
+        if rank != 0:
+            dist.barrier()
+            dist.barrier()
+            return
     import numpy as np
     import paper_2507_06608_b200 as nx
     from paper_2507_06608_b200 import device as D
 
     page_tokens = 16
-    num_pages = int(args.kv_gb * (1 << 30) // (page_tokens * MODELS[args.model][1]))
+    num_pages = int(args.kv_gb * (1 << 30) * tp // (page_tokens * MODELS[args.model][1]))
+    tp_mode = D.NX_TP_PEER_COLOCATED if args.tp_colocated else D.NX_TP_PEER
     dev = D.Device(D.arch_preset(args.model), num_pages=num_pages, page_tokens=page_tokens,
                    max_prefill_tokens=2048 + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
-                   green_contexts=not args.no_green,
-                   seed=args.seed, device=local)
+                   green_contexts=not args.no_green and not (tp > 1 and args.tp_colocated),
+                   seed=args.seed, device=0 if tp > 1 else local,
+                   **(dict(tp_size=tp, tp_mode=tp_mode) if tp > 1 else {}))
     dev.set_profiling(args.profile_every)
+    group_world = 1 if tp > 1 else world  # ranks whose results are aggregated
+
     def cfg_for(engine):
         return make_cfg(nx, engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext,
-                        args.max_decode_batch, args.alpha, args.beta, args.model, args.gamma, args.static_r_p)
+                        args.max_decode_batch, args.alpha, args.beta, args.model, args.gamma, args.static_r_p, tp)
 
     cfg = cfg_for(args.engine)
     vocab = dev.arch.vocab
@@ -420,7 +447,9 @@ def main():
     span = sum(r["makespan"] for r in results)
     window = sum(r["window"] for r in results)
     wall = sum(r["wall"] for r in results)
-    if dist:
+    if dist and tp > 1:
+        dist.barrier()
+    if dist and tp == 1:
         import torch
         t = torch.tensor([good, out_tok, span, window], dtype=torch.float64)
         w = torch.tensor([wall, window], dtype=torch.float64)
@@ -434,7 +463,7 @@ def main():
     value = good / window_max if window_max else 0.0
     # client view: the same good tokens over the wall time of submit + serve +
     # read-back, restricted to the arrival window share of that wall time
-    e2e = good / (wall_max * window_max / (span_sum / world)) if wall_max and span_sum else 0.0
+    e2e = good / (wall_max * window_max / (span_sum / group_world)) if wall_max and span_sum else 0.0
     ttft = [x for r in results for x in r["ttft"]]
     tbt = [x for r in results for x in r["tbt"]]
 
@@ -526,11 +555,12 @@ def main():
     except Exception as e:  # the baseline is reported, never required
         cpu = {"unavailable": str(e)}
     line = {
-        "metric": "goodput_tok_per_s_at_slo", "value": value, "unit": "tok/s", "n_gpus": world,
+        "metric": "goodput_tok_per_s_at_slo", "value": value, "unit": "tok/s",
+        "n_gpus": world if tp == 1 else (1 if args.tp_colocated else tp),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, sharegpt-shaped lengths, random prompt ids)",
-        "config": {"workload": f"{args.model} bf16, 1 B200 per rank, {args.workload} trace"
+        "config": {"workload": f"{args.model} bf16, " + (f"TP={tp} group" if tp > 1 else "1 B200 per rank") + f", {args.workload} trace"
                                + (" (BASELINE configs[1])" if args.model == "llama3-8b" and args.workload == "sharegpt" else ""),
                    "rate_rps": args.rate, "requests_per_step": args.requests, "engine": args.engine,
                    "seed": args.seed, "static_r_p": args.static_r_p if args.engine == "static" else None,
@@ -539,14 +569,16 @@ def main():
                    "bw_ext": not args.no_bw_ext,
                    "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt},
                    "max_decode_batch": args.max_decode_batch, "alpha": args.alpha, "beta": args.beta, "gamma": args.gamma,
-                   "kv_pool_gb": args.kv_gb, "parallelism": f"replicas x{world}",
+                   "kv_pool_gb": args.kv_gb,
+                   "parallelism": (f"tp{tp}" + (" colocated on one GPU" if args.tp_colocated else " (peer-memory all-reduce)"))
+                   if tp > 1 else f"replicas x{world}",
                    "l2": "inputs > L2 (16 GB weights streamed per decode step)"},
         "ttft_p50": nearest_rank(ttft, 50), "ttft_p99": nearest_rank(ttft, 99),
         "tbt_p50": nearest_rank(tbt, 50), "tbt_p99": nearest_rank(tbt, 99),
         "completed": sum(r["completed"] for r in results), "good_tokens": good,
         "output_tokens": out_tok, "slo_attainment": good / out_tok if out_tok else 0.0,
-        "throughput_makespan": out_tok / (span_sum / world) if span_sum else 0.0,
-        "goodput_makespan": good / (span_sum / world) if span_sum else 0.0,
+        "throughput_makespan": out_tok / (span_sum / group_world) if span_sum else 0.0,
+        "goodput_makespan": good / (span_sum / group_world) if span_sum else 0.0,
         "same_kernel_baselines": baselines,
         "decisions": sum(r["decisions"] for r in results), "switches": sum(r["switches"] for r in results),
         "r_p_hist_arrivals": {str(k): sum(r["r_p_hist"].get(k, 0) for r in results)

@@ -112,7 +112,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hkv = g.n_kv_heads, G = g.group;
-  pdl_trigger();
   if (warp == 0 && lane == 0) {
     tma_prefetch(&qmap);
     mbar_init(q_full, 1);
@@ -138,6 +137,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // Dependents may launch only once every CTA of this grid holds its TMEM: a
+  // dependent CTA co-resident on an SM could otherwise allocate first and
+  // spin in griddepcontrol.wait while this CTA blocks in tcgen05.alloc.
+  pdl_trigger();
   pdl_wait();  // q / k / v of this chunk come from the QKV projection
 
   if (warp == 0) {

@@ -113,7 +113,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
-  pdl_trigger();
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tx);
     for (int s = 0; s < kStages; ++s) {
@@ -131,6 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Dependents may launch only once every CTA of this grid holds its TMEM: a
+  // dependent CTA co-resident on an SM could otherwise allocate first and
+  // spin in griddepcontrol.wait while this CTA blocks in tcgen05.alloc.
+  pdl_trigger();
 
   if (warp == 0) {
     // ---------------- producer ----------------

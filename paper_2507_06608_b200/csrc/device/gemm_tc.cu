@@ -450,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) NX_STAMP(0);
-  pdl_trigger();  // let the next kernel's CTAs stage their prologue early
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tx);
     for (int s = 0; s < C::kStages; ++s) {
@@ -469,6 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Dependents may launch only once every CTA of this grid holds its TMEM: a
+  // dependent CTA co-resident on an SM could otherwise allocate first and
+  // spin in griddepcontrol.wait while this CTA blocks in tcgen05.alloc.
+  pdl_trigger();
   if (threadIdx.x == 0) NX_STAMP(1);
 
   if (warp == 0) {
