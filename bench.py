@@ -229,13 +229,16 @@ def dist_setup(args):
 
 
 def load_calib(base):
-    """(peak_compute, peak_bandwidth, profile, bw_sat) from a calibration, or None."""
+    """(peak_compute, peak_bandwidth, profile, bw_sat, contention (c0, c1) or
+    None) from a calibration, or None."""
     if not base or base == "none" or not os.path.exists(base + ".json"):
         return None
     import paper_2507_06608_b200 as nx
     d = json.load(open(base + ".json"))
     prof, _ = nx.parse_kernel_profile(open(base + ".calib").read())
-    return d["gpu_spec"]["peak_compute"], d["gpu_spec"]["peak_bandwidth"], prof, d["bw_sat"]
+    cf = d.get("contention_fit")
+    return (d["gpu_spec"]["peak_compute"], d["gpu_spec"]["peak_bandwidth"], prof, d["bw_sat"],
+            (cf["c0"], cf["c1"], cf.get("c2", 0.0)) if cf else None)
 
 
 def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True, max_decode_batch=64,
@@ -246,7 +249,7 @@ def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True,
     slack = 4096
     cap_tokens = (num_pages - slack) * page_tokens
     cal = load_calib(calib)
-    C, B, prof, bw_sat = (1.6595e15, 6.5562e12, None, None) if cal is None else cal
+    C, B, prof, bw_sat, cont = (1.6595e15, 6.5562e12, None, None, None) if cal is None else cal
     g = nx.gpu_spec(148, C * tp, B * tp, cap_tokens * ref_kvbpt(model))
     kind = {"nexus": nx.NX_ENGINE_NEXUS, "static": nx.NX_ENGINE_STATIC,
             "monolithic": nx.NX_ENGINE_MONOLITHIC}[engine]
@@ -256,7 +259,8 @@ def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True,
     if gamma is not None:
         ctrl.gamma = gamma
     return nx.sim_config(m, g, kind=kind, clock_mode=clock_mode, profile=prof, ctrl=ctrl,
-                         bw_sat=bw_sat if bw_ext else None, static_r_p=static_r_p)
+                         bw_sat=bw_sat if bw_ext else None, static_r_p=static_r_p,
+                         contention=cont if bw_ext else None)
 
 
 def reference_cfg(args, num_pages, page_tokens, engine=None):

@@ -128,8 +128,13 @@ typedef struct nx_engine_config {
  * its controller starve decode of SMs. */
 typedef struct nx_cost_ext {
   int32_t enabled;
-  int32_t _pad0;
+  int32_t contention; /* 1: co-located decode = isolated x (c0 + c1 p + c2 p^2), p = prefill share */
   double bw_sat[5]; /* per operator kind, in (0, 1] */
+  /* Measured co-location slowdown of a decode batch beside a prefill batch
+   * (paper_2507_06608_b200.calibrate), replacing the B_decode bandwidth split
+   * (costmodel.cpp:56-64) when `contention` is set: on B200 the shared power
+   * / clock budget, not HBM bandwidth, dominates the slowdown. */
+  double contention_c[3];
 } nx_cost_ext;
 
 /* SimConfig (simulator.hpp:45-51) + the cost-model extension. */
@@ -581,6 +586,12 @@ typedef struct nx_kernel_stats {
   uint64_t kernel_launches; /* every kernel this device launched (all batches) */
   uint64_t batches;         /* every batch this device ran */
   double sm_ms[NX_K_CLASSES]; /* sum of (lane SM count x event ms): / ms = mean partition size */
+  /* the same sampled event time charged to the reference operator a kernel
+   * belongs to (NX_OP_*: the projection GEMM with its norm / fold / RoPE /
+   * all-reduce kernels, or the attention); embedding, lm_head and sampling
+   * are not operators of the cost model and are not charged */
+  double op_ms[5];
+  uint64_t op_launches[5];
 } nx_kernel_stats;
 int nx_device_set_profiling(nx_device* dev, int32_t sample_every);
 int nx_device_kernel_stats(const nx_device* dev, nx_kernel_stats* out);

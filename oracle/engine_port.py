@@ -112,7 +112,12 @@ def breakdown(ops, share, gpu, prof, dbw=0.0, ext=None):  # costmodel.cpp:18-41
     return total, attn
 
 
-def contended(dops, share, pbd, pops, gpu, prof, ext=None):  # costmodel.cpp:66-96
+def contended(dops, share, pbd, pops, gpu, prof, ext=None, cont=None):  # costmodel.cpp:66-96
+    if cont is not None:  # the product's flagged measured-slowdown form (model_cost.cpp decode_contended)
+        t, a = breakdown(dops, share, gpu, prof, 0.0, ext)
+        pp = 1.0 - share
+        f = cont[0] + cont[1] * pp + cont[2] * pp * pp
+        return t * f, a * f
     p = 0.0 if pbd[0] <= 0 else pbd[1] / pbd[0]
     m_p1 = m_p2 = m_d = 0.0
     for kind, fl, mem, kv, is_attn in pops:
@@ -232,6 +237,7 @@ def run_port(cfg, trace, replay=None):
     the cost-model latency of the k-th launch by replay[k]."""
     m, gpu, ctrl, prof, eng = cfg.model, cfg.gpu, cfg.ctrl, cfg.profile, cfg.engine
     ext = list(cfg.ext.bw_sat) if cfg.ext.enabled else None
+    cont = list(cfg.ext.contention_c) if cfg.ext.enabled and cfg.ext.contention else None
     kind = eng.kind  # 0 nexus, 1 monolithic, 2 static
     dynamic, mono = kind == 0, kind == 1
     ctl = Controller(eng.static_r_p if kind == 2 else 50, ctrl)
@@ -325,7 +331,7 @@ def run_port(cfg, trace, replay=None):
         ops = decode_ops(m, ctxs(ms))
         r_p = decide(False, ops) if dynamic else ctl.r_p
         share = (100 - r_p) / 100.0
-        D.bd = (contended(ops, share, P.bd, P.ops, gpu, prof, ext) if P.busy
+        D.bd = (contended(ops, share, P.bd, P.ops, gpu, prof, ext, cont) if P.busy
                 else breakdown(ops, share, gpu, prof, 0.0, ext))
         D.dec, D.pre, D.ops, D.r_p = ms, [], ops, r_p
         begin(D, "decode", D.bd[0])

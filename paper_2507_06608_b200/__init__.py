@@ -89,9 +89,13 @@ def sim_config(model: ModelConfig, gpu: GpuSpec, *, kind: int = NX_ENGINE_NEXUS,
                static_r_p: int = 50, prefill_policy: int = NX_PREFILL_SPF,
                clock_mode: int = NX_CLOCK_VIRTUAL, ctrl: ControllerConfig | None = None,
                profile: KernelProfile | None = None, timeout_sim_s: float = 3600.0,
-               max_events: int = 10_000_000, bw_sat: Sequence[float] | None = None) -> SimConfig:
+               max_events: int = 10_000_000, bw_sat: Sequence[float] | None = None,
+               contention: Sequence[float] | None = None) -> SimConfig:
     """SimConfig; bw_sat (5 per-op shares) enables the SM-share-limited HBM
-    bandwidth extension of the cost model (nx_cost_ext), None = reference."""
+    bandwidth extension of the cost model (nx_cost_ext), None = reference;
+    contention (c0, c1[, c2]) additionally replaces the contended-decode
+    bandwidth split by the measured slowdown c0 + c1 p + c2 p^2 (p = the
+    prefill lane's share)."""
     cfg = SimConfig()
     cfg.model = model
     cfg.gpu = gpu
@@ -102,16 +106,21 @@ def sim_config(model: ModelConfig, gpu: GpuSpec, *, kind: int = NX_ENGINE_NEXUS,
     e.timeout_sim_s, e.max_events = timeout_sim_s, max_events
     cfg.engine = e
     if bw_sat is not None:
-        cfg.ext = CostExt(1, 0, (C.c_double * 5)(*bw_sat))
+        cfg.ext = _ext(bw_sat, contention)
     return cfg
 
 
-def set_cost_ext(bw_sat: Sequence[float] | None) -> None:
+def _ext(bw_sat, contention=None) -> CostExt:
+    c = (0.0, 0.0, 0.0) if contention is None else tuple(contention) + (0.0,) * (3 - len(contention))
+    return CostExt(1, 0 if contention is None else 1, (C.c_double * 5)(*bw_sat), (C.c_double * 3)(*c))
+
+
+def set_cost_ext(bw_sat: Sequence[float] | None, contention: Sequence[float] | None = None) -> None:
     """Extension for the standalone cost-model calls (phase_latency_isolated, ...)."""
     if bw_sat is None:
         _check(lib().nx_set_cost_ext(None))
     else:
-        _check(lib().nx_set_cost_ext(C.byref(CostExt(1, 0, (C.c_double * 5)(*bw_sat)))))
+        _check(lib().nx_set_cost_ext(C.byref(_ext(bw_sat, contention))))
 
 
 def validate_config(model, gpu, ctrl, prof) -> list[str]:

@@ -62,7 +62,8 @@ class EngineConfig(C.Structure):
 
 
 class CostExt(C.Structure):
-    _fields_ = [("enabled", C.c_int32), ("_pad0", C.c_int32), ("bw_sat", C.c_double * 5)]
+    _fields_ = [("enabled", C.c_int32), ("contention", C.c_int32), ("bw_sat", C.c_double * 5),
+                ("contention_c", C.c_double * 3)]
 
 
 class SimConfig(C.Structure):

@@ -48,7 +48,8 @@ class KernelStats(C.Structure):
     _fields_ = [("ms", C.c_double * 5), ("bytes", C.c_double * 5), ("flops", C.c_double * 5),
                 ("launches", C.c_uint64 * 5), ("batches_sampled", C.c_uint64),
                 ("batch_ms_sampled", C.c_double), ("kernel_launches", C.c_uint64),
-                ("batches", C.c_uint64), ("sm_ms", C.c_double * 5)]
+                ("batches", C.c_uint64), ("sm_ms", C.c_double * 5), ("op_ms", C.c_double * 5),
+                ("op_launches", C.c_uint64 * 5)]
 
 
 PROTOS = {

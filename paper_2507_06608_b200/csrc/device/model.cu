@@ -531,6 +531,7 @@ void Model::forward(LaneWs& ws) {
   cudaStream_t s = ws.stream;
   // Sampled profiling: an event pair around each launch, with its
   // algorithmic bytes / FLOPs, folded into kstats_ when the batch finishes.
+  int op = -1;  // reference operator (NX_OP_*) the next launches belong to; -1 = none
   auto timed = [&](int kind, double bytes, double flops, auto&& fn) {
     if (!ws.prof || ws.ev_used + 2 > ws.ev_pool.size()) {
       fn();
@@ -540,7 +541,7 @@ void Model::forward(LaneWs& ws) {
     cudaEventRecord(a, s);
     fn();
     cudaEventRecord(b, s);
-    ws.recs.push_back({kind, a, b, bytes, flops});
+    ws.recs.push_back({kind, op, a, b, bytes, flops});
   };
   const int T = ws.tokens;
   const double Td = T;
@@ -594,6 +595,7 @@ void Model::forward(LaneWs& ws) {
     rope.n_heads = hq_;
     rope.n_kv_heads = hkv_;
     rope.page_tokens = cfg_.page_tokens;
+    op = NX_OP_QKV_PROJ;
     if (!fold || l == 0)
       timed(NX_K_OTHER, Td * d * 4, 0, [&] {
         ck(rmsnorm(ws.x, nullptr, T, d, w.attn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
@@ -620,6 +622,7 @@ void Model::forward(LaneWs& ws) {
                          cfg_.page_tokens, kplane, vplane, s),
            "rope");
       });
+    op = NX_OP_ATTN_DECODE;
     if (ws.dec_seq_count > 0)
       timed(NX_K_ATTN_DECODE, ws.dec_kv_tokens * kvtok + ws.dec_seq_count * qo,
             4.0 * ws.dec_kv_tokens * attn_cols_, [&] {
@@ -628,6 +631,7 @@ void Model::forward(LaneWs& ws) {
                                   ws.attn, ws.part_o, ws.part_ml, ws.part_cap, sm, s),
                  "decode attention");
             });
+    op = NX_OP_ATTN_PREFILL;
     if (ws.n_work > 0)
       timed(NX_K_ATTN_PREFILL, ws.pre_kv_tokens * kvtok + (Td - ws.dec_seq_count) * qo,
             4.0 * ws.pre_pairs * attn_cols_, [&] {
@@ -638,6 +642,7 @@ void Model::forward(LaneWs& ws) {
     // Row-parallel under TP: rank 0 adds the residual, the others store
     // their partial; the all-reduce then yields x + sum_r o_r on every rank.
     const int res_mode = (tp_ == 1 || rank_ == 0) ? kEpiResidual : kEpiStore;
+    op = NX_OP_ATTN_OUT_PROJ;
     timed(gk, gbytes(d, attn_cols_, fold ? 4 : 2, !fold), gflops(d, attn_cols_), [&] {
       ck(fold ? gemm_decode(w.o, ws.map_attn[bi], bn, d, T, attn_cols_, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fo)
               : pair ? gemm_pair(w.o, ws.map_attn[2], d, T, attn_cols_, res_mode, ws.x, d, nullptr, ws.x, d, sm, s)
@@ -654,6 +659,7 @@ void Model::forward(LaneWs& ws) {
       timed(NX_K_OTHER, Td * d * 4, 0, [&] {
         ck(rmsnorm(ws.x, nullptr, T, d, w.ffn_norm, a_.rms_eps, ws.h, s), "rmsnorm");
       });
+    op = NX_OP_FFN;
     timed(gk, gbytes(2.0 * ffn_, d, fold ? 8 : 1, false), gflops(2.0 * ffn_, d), [&] {
       ck(fold ? gemm_decode(w.gate_up, ws.map_h[bi], bn, 2 * ffn_, T, d, nullptr, 0, ws.ws, ws.ws_bytes, sm, s, &fg)
               : pair ? gemm_pair(w.gate_up, ws.map_h[2], 2 * ffn_, T, d, kEpiSwiGLU, ws.act, ffn_, nullptr, nullptr, 0,
@@ -682,6 +688,7 @@ void Model::forward(LaneWs& ws) {
       });
     }
   }
+  op = -1;
   // lm_head over the sampled rows, in chunks of the logits buffer.
   ws.d_out_tokens = ws.logits_tokens_dev();
   for (int r0 = 0; r0 < ws.n_sample; r0 += ws.sample_cap) {
@@ -770,6 +777,10 @@ void Model::finish(LaneWs& ws) {
       kstats_.bytes[r.kind] += r.bytes;
       kstats_.flops[r.kind] += r.flops;
       kstats_.launches[r.kind] += 1;
+      if (r.op >= 0) {
+        kstats_.op_ms[r.op] += t;
+        kstats_.op_launches[r.op] += 1;
+      }
     }
     kstats_.batches_sampled += 1;
     kstats_.batch_ms_sampled += ms;

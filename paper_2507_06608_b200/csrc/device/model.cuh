@@ -90,7 +90,7 @@ struct LaneWs {
   float last_ms = 0.f;
   // sampled per-kernel-class profiling
   struct ProfRec {
-    int kind;
+    int kind, op;
     cudaEvent_t a, b;
     double bytes, flops;
   };

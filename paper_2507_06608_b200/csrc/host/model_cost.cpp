@@ -295,6 +295,19 @@ nx_breakdown decode_contended(const OpList& dec, double share, const nx_breakdow
                               const OpList& pre, const nx_gpu_spec& g,
                               const nx_kernel_profile& p, const nx_cost_ext* ext) {
   if (pre_bd == nullptr) return isolated(dec, share, g, p, ext);
+  if (ext != nullptr && ext->enabled != 0 && ext->contention != 0) {
+    // measured co-location slowdown vs the prefill lane's share (flagged ext)
+    nx_breakdown b = isolated(dec, share, g, p, ext);
+    const double pp = 1.0 - share;
+    const double f = ext->contention_c[0] + ext->contention_c[1] * pp + ext->contention_c[2] * pp * pp;
+    for (int i = 0; i < b.n_ops; ++i) {
+      b.per_op[i].compute_s *= f;
+      b.per_op[i].mem_s *= f;
+    }
+    b.total_s *= f;
+    b.attn_mem_time_s *= f;
+    return b;
+  }
   const double p_attn = pre_bd->total_s <= 0 ? 0.0 : pre_bd->attn_mem_time_s / pre_bd->total_s;
   double m_p1 = 0, m_p2 = 0, m_d = 0;
   for (int i = 0; i < pre.n; ++i) {

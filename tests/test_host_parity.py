@@ -351,3 +351,32 @@ def test_c1_trace_file_golden(nx):
     text = open(os.path.join(os.path.dirname(__file__), "golden", "c1_mixed_64_2.5rps_seed1.trace")).read()
     assert nx.trace_text(nx.workload_trace("mixed", 2.5, 64, 1)) == text
     assert nx.trace_text(nx.parse_trace(text)) == text
+
+
+def test_contention_ext_engine_matches_port(nx):
+    """The flagged measured-contention term (nx_cost_ext.contention): the
+    co-located decode prediction becomes isolated x (c0 + c1 p + c2 p^2);
+    the product engine and the Python port agree byte for byte, and the term
+    changes the predicted timeline versus the bandwidth-only extension."""
+    from oracle.engine_port import run_port
+    m = nx.model_preset("8b")
+    g = nx.gpu_spec(148, 1.3e15, 5.5e12, 150 << 30)
+    trace = nx.workload_trace("sharegpt", 40.0, 200, 7)
+    bw = [0.45] * 5
+    plain = nx.sim_config(m, g, bw_sat=bw)
+    cont = nx.sim_config(m, g, bw_sat=bw, contention=[1.05, 0.3, -0.1])
+    r = nx.run(cont, trace)
+    ev, dec = run_port(cont, trace)
+    assert r.event_log == ev and r.decision_log == dec
+    assert r.event_log != nx.run(plain, trace).event_log
+    ops = nx.decode_op_workloads(m, [600] * 64)
+    pops = nx.prefill_batch_workloads(m, [(512, 512)] * 4)
+    prof = nx.lib().nx_kernel_profile_default()
+    nx.set_cost_ext(bw, [1.05, 0.3, -0.1])
+    try:
+        iso = nx.phase_latency_isolated(ops, 0.25, g, prof).total_s
+        pbd = nx.phase_latency_isolated(pops, 0.75, g, prof)
+        co = nx.decode_latency_contended(ops, 0.25, pbd, pops, g, prof).total_s
+    finally:
+        nx.set_cost_ext(None)
+    assert abs(co / iso - (1.05 + 0.3 * 0.75 - 0.1 * 0.75 ** 2)) < 1e-12

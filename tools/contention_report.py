@@ -24,6 +24,21 @@ def main(base):
         report(cal, m, gpu, prof)
     finally:
         nx.set_cost_ext(None)  # process-wide switch: leave the reference form on
+    cf = cal.get("contention_fit")
+    if cf:
+        report_fit(cal, cf)
+
+
+def report_fit(cal, cf):
+    c2 = cf.get("c2", 0.0)
+    print("\nFitted measured-contention term (nx_cost_ext.contention, flagged): slowdown = "
+          f"{cf['c0']:.4f} + {cf['c1']:.4f} p + {c2:.4f} p^2, p = prefill share\n")
+    print("| decode SMs | prefill share | measured slowdown | fitted slowdown | rel. error |")
+    print("|---|---|---|---|---|")
+    for c in cal["contention"]:
+        p = c["prefill_sms"] / (c["prefill_sms"] + c["decode_sms"])
+        f = cf["c0"] + cf["c1"] * p + c2 * p * p
+        print(f"| {c['decode_sms']} | {p:.3f} | {c['slowdown']:.3f} | {f:.3f} | {f / c['slowdown'] - 1:+.3f} |")
 
 
 def report(cal, m, gpu, prof):
