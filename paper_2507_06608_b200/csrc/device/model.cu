@@ -49,6 +49,7 @@ void Partitions::init(int device, bool enable) {
   // (same kernels, no SM partitions) unless NX_GREEN_UNDER_PROFILER=1.
   const bool profiler = std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
                         std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") || std::getenv("CUDA_INJECTION64_PATH");
+  if (const char* e = std::getenv("NX_GREEN"); e && e[0] == '0') enable = false;  // plain streams (tools)
   if (enable && profiler && !std::getenv("NX_GREEN_UNDER_PROFILER")) {
     std::fprintf(stderr, "nexus_b200: profiler injection detected, green-context partitions disabled\n");
     enable = false;
