@@ -357,214 +357,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 
-// ---------------------------------------------------------------------------
-// Ping-pong variant: two 128-row Q tiles (a, b) per item share every K / V
-// tile, each with its own softmax warpgroup, score buffer and O accumulator
-// in TMEM (S_a, S_b, O_a, O_b = 512 columns). The tensor pipe alternates
-// QK_a, QK_b, PV_a, PV_b, so one warpgroup's softmax runs while the other
-// tile's MMAs execute, two softmax warps share each SM sub-partition (latency
-// hiding the single-warpgroup kernel lacks), and K / V shared-memory traffic
-// per FLOP halves. Warps 0-3 softmax a, 4-7 softmax b, 8 producer, 9 MMA.
-// ---------------------------------------------------------------------------
-constexpr int kPPThreads = 320;
-constexpr int kPPRows = 256;
-constexpr uint32_t kPPQHalf = kPPRows * 128;       // 32 KB
-constexpr int kPPKStages = 3, kPPVStages = 2;
-constexpr uint32_t kPPSmemMain = 2 * kPPQHalf + (kPPKStages + kPPVStages) * kKVBytes;
-constexpr size_t kPPSmemTotal = kPPSmemMain + 1024 + 256;
-
-__global__ void __maxnreg__(200)
-    prefill_attn_pp_kernel(AttnGeom g, const __grid_constant__ CUtensorMap qmap,
-                           const __nv_bfloat16* __restrict__ kvplane, const AttnSeq* __restrict__ seqs,
-                           const int2* __restrict__ work, int n_items, int tq, const int32_t* __restrict__ pages,
-                           __nv_bfloat16* __restrict__ out) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sq = smem;                                // [2 halves][256 rows][128 B]
-  uint8_t* sk = smem + 2 * kPPQHalf;                 // [kPPKStages][128 keys x 256 B]
-  uint8_t* sv = sk + kPPKStages * kKVBytes;          // [kPPVStages][128 keys x 256 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPPSmemMain);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* s_full = bars + 2;   // [a, b]
-  uint64_t* p_full = bars + 4;   // [a, b]
-  uint64_t* o_done = bars + 6;   // [a, b]
-  uint64_t* o_free = bars + 8;   // [a, b]
-  uint64_t* k_full = bars + 10;  // [kPPKStages]
-  uint64_t* k_empty = k_full + kPPKStages;
-  uint64_t* v_full = k_empty + kPPKStages;  // [kPPVStages]
-  uint64_t* v_empty = v_full + kPPVStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + kPPVStages);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hkv = g.n_kv_heads, G = g.group;
-  if (warp == 8 && lane == 0) {
-    tma_prefetch(&qmap);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&o_done[i], 1);
-      mbar_init(&o_free[i], 128);
-    }
-    for (int i = 0; i < kPPKStages; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < kPPVStages; ++i) {
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-  pdl_trigger();  // after the TMEM allocation (see gemm_decode.cu)
-  pdl_wait();     // q / k / v of this chunk come from the QKV projection
-
-  if (warp == 8) {
-    // ---------------- producer ----------------
-    uint32_t kv_it = 0, item_it = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_it) {
-      const Item x = get_item(it, work, seqs, hkv, tq);
-      if (lane == 0) {
-        mbar_wait(q_empty, (item_it & 1) ^ 1);
-        mbar_expect_tx(q_full, 2u * G * tq * 128u);
-        for (int h = 0; h < 2; ++h)
-          tma_load_4d(&qmap, q_full, sq + h * kPPQHalf, 0, h, x.kvh * G, x.q_start + x.tok0);
-      }
-      const int32_t* pt = pages + x.page_off;
-      const int last_page = pt[(x.kv_end - 1) >> 4];
-      for (int j = 0; j < x.n_tiles; ++j, ++kv_it) {
-        const int key = j * kKeys + (lane & 7) * 16;
-        const int page = key < x.kv_end ? pt[key >> 4] : last_page;
-        const __nv_bfloat16* src = kvplane + (static_cast<size_t>(page) * hkv + x.kvh) * kBlockElems;
-        const uint32_t ks = kv_it % kPPKStages, vs = kv_it % kPPVStages;
-        if (lane == 0) {
-          mbar_wait(&k_empty[ks], ((kv_it / kPPKStages) & 1) ^ 1);
-          mbar_expect_tx(&k_full[ks], kKVBytes);
-        }
-        __syncwarp();
-        if (lane < kPagesT) bulk_load(sk + ks * kKVBytes + lane * 4096, src, 4096, &k_full[ks]);
-        if (lane == 0) {
-          mbar_wait(&v_empty[vs], ((kv_it / kPPVStages) & 1) ^ 1);
-          mbar_expect_tx(&v_full[vs], kKVBytes);
-        }
-        __syncwarp();
-        if (lane < kPagesT) bulk_load(sv + vs * kKVBytes + lane * 4096, src + kBlockElems / 2, 4096, &v_full[vs]);
-      }
-    }
-  } else if (warp == 9) {
-    // ---------------- MMA issuer: QK_a, QK_b, then per tile PV_a, QK_a', PV_b, QK_b' ----------------
-    uint32_t kv_it = 0, gt = 0, item_it = 0;
-    const uint32_t sq_s = smem_u32(sq), sk_s = smem_u32(sk), sv_s = smem_u32(sv);
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_it) {
-      const Item x = get_item(it, work, seqs, hkv, tq);
-      if (lane == 0) {
-        const int n = x.n_tiles;
-        auto qk = [&](int t, uint32_t kst) {  // S_t = Q_t K^T
-          const uint32_t kb = sk_s + kst * kKVBytes;
-#pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            const uint32_t koff = (s >> 2) * 1024 + (s & 3) * 32;
-            const uint32_t qoff = (s >> 2) * kPPQHalf + t * kQHalf + (s & 3) * 32;
-            umma_bf16(tbase + kTmemS + t * 128, umma_desc_sw128(sq_s + qoff, 16, 1024),
-                      umma_desc_sw128(kb + koff, 16, 2048), kIdescQK, s > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[t]);
-        };
-        mbar_wait(q_full, item_it & 1);
-        {
-          const uint32_t kst = kv_it % kPPKStages;
-          mbar_wait(&k_full[kst], (kv_it / kPPKStages) & 1);
-          tc_fence_after();
-          qk(0, kst);
-          qk(1, kst);
-          umma_commit(&k_empty[kst]);
-          if (n == 1) umma_commit(q_empty);
-        }
-        for (int j = 0; j < n; ++j) {
-          const uint32_t kv = kv_it + j, gg = gt + j, vst = kv % kPPVStages;
-          mbar_wait(&v_full[vst], (kv / kPPVStages) & 1);
-          const uint32_t vb = sv_s + vst * kKVBytes;
-          const uint32_t kn = (kv + 1) % kPPKStages;
-          for (int t = 0; t < 2; ++t) {
-            mbar_wait(&p_full[t], gg & 1);
-            if (j == 0 && item_it > 0) mbar_wait(&o_free[t], (item_it - 1) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int s = 0; s < kPagesT; ++s)
-              umma_bf16_ts(tbase + kTmemO + t * 128, tbase + kTmemS + t * 128 + 8 * s,
-                           umma_desc_sw128(vb + s * 4096, 1024, 2048), kIdescPV, (j > 0 || s > 0) ? 1u : 0u);
-            umma_commit(&o_done[t]);
-            if (t == 1) umma_commit(&v_empty[vst]);
-            if (j + 1 < n) {
-              if (t == 0) {
-                mbar_wait(&k_full[kn], ((kv + 1) / kPPKStages) & 1);
-                tc_fence_after();
-              }
-              qk(t, kn);
-              if (t == 1) {
-                umma_commit(&k_empty[kn]);
-                if (j + 2 == n) umma_commit(q_empty);
-              }
-            }
-          }
-        }
-        kv_it += n;
-        gt += n;
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- softmax + epilogue, one warpgroup per Q tile ----------------
-    const int t = warp >> 2;                // Q tile of this warpgroup
-    const int q = warp & 3;                 // TMEM lane quarter
-    const int r = t * 128 + q * 32 + lane;  // query row within the item
-    const uint32_t trow = tbase + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t ts = trow + kTmemS + t * 128, to = trow + kTmemO + t * 128;
-    uint32_t gt = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const Item x = get_item(it, work, seqs, hkv, tq);
-      const int tk = x.tok0 + r / G;
-      const bool valid = r < G * tq && tk < x.q_len;
-      const int limit = valid ? x.start + tk : -1;
-      float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < x.n_tiles; ++j, ++gt) {
-        mbar_wait(&s_full[t], gt & 1);
-        tc_fence_after();
-        softmax_tile(ts, to, j, limit, g.scale_log2, &o_done[t], gt, m, l);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&p_full[t]);
-      }
-      mbar_wait(&o_done[t], (gt - 1) & 1);
-      tc_fence_after();
-      store_rows(to, valid, l,
-                 out + static_cast<size_t>(x.q_start + tk) * g.out_stride + (x.kvh * G + r % G) * kHD);
-      tc_fence_before();
-      mbar_arrive(&o_free[t]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc<512>(tbase);
-  }
-}
-
-bool pingpong_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("NX_ATTN_PP");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
 }  // namespace
 
 bool encode_q_heads_map(CUtensorMap* map, const void* qkv, int tokens, int n_heads, int group,
@@ -588,7 +380,7 @@ bool encode_q_heads_map(CUtensorMap* map, const void* qkv, int tokens, int n_hea
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int prefill_attn_tokens_per_item(int group) { return (pingpong_enabled() ? kPPRows : kRows) / group; }
+int prefill_attn_tokens_per_item(int group) { return kRows / group; }
 
 cudaError_t prefill_attention(const AttnGeom& g, const CUtensorMap& qmap, const __nv_bfloat16* kvplane,
                               const AttnSeq* seqs, const int2* work, int n_work, const int32_t* pages,
@@ -599,20 +391,13 @@ cudaError_t prefill_attention(const AttnGeom& g, const CUtensorMap& qmap, const 
   const int n_items = n_work * g.n_kv_heads;
   const int grid = std::max(1, std::min(n_items, sm_count));
   ++g_kernel_launches;
-  if (pingpong_enabled())
-    return launch_pdl(prefill_attn_pp_kernel, dim3(grid), dim3(kPPThreads), kPPSmemTotal, s, g, qmap, kvplane,
-                      seqs, work, n_items, prefill_attn_tokens_per_item(g.group), pages, out);
   return launch_pdl(prefill_attn_tc_kernel, dim3(grid), dim3(kThreads), kSmemTotal, s, g, qmap, kvplane, seqs,
                     work, n_items, prefill_attn_tokens_per_item(g.group), pages, out);
 }
 
 cudaError_t prepare_prefill_attention_kernel() {
-  cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kSmemTotal));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(prefill_attn_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kPPSmemTotal));
-  return e;
+  return cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kSmemTotal));
 }
 
 }  // namespace nxd
