@@ -121,7 +121,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t ts, uint32_t to, int j, in
   const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
   const float mnew = mx * scale_log2;  // -inf stays -inf
   const bool resc = mnew > m + 8.f;
-  if (__any_sync(0xffffffffu, resc && j > 0)) {
+  const bool rescale_o = __any_sync(0xffffffffu, resc && j > 0);
+  if (rescale_o) {
     mbar_wait(o_done, (gt - 1) & 1);
     tc_fence_after();
     const float alpha = (resc && j > 0) ? ex2(m - mnew) : 1.f;
@@ -158,6 +159,10 @@ __device__ __forceinline__ void softmax_tile(uint32_t ts, uint32_t to, int j, in
     tmem_st32(ts + 32 * c, v[2 * c]);
   }
   l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+  // every PV completion is observed exactly once (here, in the rescale above,
+  // or in the epilogue for the item's last tile): by the end of this tile's
+  // softmax PV_{j-1} has normally landed, so the wait costs nothing
+  if (j > 0 && !rescale_o) mbar_wait(o_done, (gt - 1) & 1);
 }
 
 // Epilogue of one query row: O / l from TMEM -> 128 bf16 (skipped for rows
