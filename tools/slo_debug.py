@@ -52,3 +52,24 @@ for rid, ts in times.items():
             big = [round(g * 1e3, 1) for g in gaps[-5:]]
             print("miss", rid, "tokens", len(ts), "ttft", round(tt, 3), "largest gaps ms", big)
 print("requests", len(times), "miss_ttft", miss_ttft, "miss_tbt", miss_tbt, "miss by output length bucket", sorted(hist.items()))
+
+# prefill-lane composition: tokens per prefill (or mixed) batch, its latency, lane busy time
+sizes, lats, dec_rows, busy = [], [], [], 0.0
+for line in eng.event_log().splitlines():
+    c = line.split("\t")
+    if c[2] != "launch" or c[1] not in ("prefill", "mixed"):
+        continue
+    pre = d = 0
+    for m in c[3].split(","):
+        rid, tok, _ = (int(x) for x in m.split(":"))
+        if c[1] == "prefill" or tok > 1:
+            pre += tok
+        else:
+            d += 1
+    sizes.append(pre)
+    dec_rows.append(d)
+    lats.append(float(c[6]) if len(c) > 6 else 0.0)
+sizes_s = sorted(sizes)
+print("prefill-lane batches", len(sizes), "mean prefill tokens", round(sum(sizes) / len(sizes)), "p50", sizes_s[len(sizes) // 2],
+      "mean decode rows", round(sum(dec_rows) / len(dec_rows), 1), "mean latency ms", round(1e3 * sum(lats) / len(lats), 2),
+      "busy s", round(sum(lats), 2))
