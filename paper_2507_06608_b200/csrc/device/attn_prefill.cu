@@ -4,28 +4,30 @@
 // Work item = (sequence, 128 query rows, kv head). A query row is a (token,
 // head-in-GQA-group) pair, row R = token * G + g, so the G heads that share a
 // kv head share every staged K/V tile; a tile holds tq = 128 / G tokens.
-// The CTA is persistent over items (host-sorted longest first) and runs six
+// The CTA is persistent over items (host-sorted longest first) and runs ten
 // warps:
 //   warp 0   producer: Q tile by one 4D TMA per 64-dim half (straight from the
 //            qkv activations, RoPE already applied by the QKV epilogue), K / V
 //            tiles of 128 keys as 8 + 8 cp.async.bulk copies of 4 KB (one per
 //            page) into separate 3-stage K and V rings (a K stage frees as soon
-//            as S = Q K^T lands, so loads run ahead of the softmax). The cache's atom layout
-//            (kv_chunk_elem) makes 8 consecutive K (V) page halves one
-//            uniform UMMA operand.
+//            as S = Q K^T lands). The cache's atom layout (kv_chunk_elem) makes
+//            8 consecutive K (V) page halves one uniform UMMA operand.
 //   warp 1   MMA issuer: S_j = Q K_j^T (SS, K-major, M 128 x N 128 x K 128)
 //            into one of two TMEM score buffers, then O += P_{j-1} V_{j-1}
 //            (TS: P read from TMEM where softmax left it, V MN-major from
 //            shared memory), so the scores of tile j are computed while the
 //            softmax warps work on tile j - 1.
-//   warps 2-5 softmax + epilogue, one thread per query row (TMEM lane):
-//            tcgen05.ld the 128 scores, causal mask, running max in the exp2
-//            domain, P = 2^(s - m) written back over the scores as bf16 pairs
+//   warps 2-9 softmax + epilogue, two threads per query row (TMEM lane): warps
+//            2-5 own columns 0-63, warps 6-9 columns 64-127 of their lane
+//            quarter; the row max and the final sum are swapped through spare
+//            TMEM columns around a named barrier of the warp pair. tcgen05.ld
+//            the scores, causal mask, running max in the exp2 domain,
+//            P = 2^(s - m) written back over the scores as bf16 pairs
 //            (tcgen05.st). The O accumulator is rescaled only when a row's
 //            max grows by more than 2^8 (the final division by l uses the
 //            same stale max, so the result is exact); the epilogue divides
 //            by l and stores bf16 rows.
-// TMEM: S0 [0, 128), S1 [128, 256), O [256, 384) columns (512 allocated).
+// TMEM: S0 [0, 128), S1 [128, 256), O [256, 384), exchange [384, 390) (512 allocated).
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -46,7 +48,7 @@ constexpr int kKeys = 128;                     // keys per K / V tile
 constexpr int kPagesT = kKeys / 16;            // pages per tile
 constexpr int kKStages = 3;                     // K ring (freed as soon as S = Q K^T lands)
 constexpr int kVStages = 3;                     // V ring (freed after O += P V)
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // producer, MMA, 8 softmax warps (two per query row)
 constexpr uint32_t kQHalf = kRows * 128;       // 16 KB: 128 rows x 64 dims
 constexpr uint32_t kKVBytes = kKeys * kHD * 2; // 32 KB: K (or V) of one tile
 constexpr uint32_t kSmemMain = 2 * kQHalf + (kKStages + kVStages) * kKVBytes;
@@ -88,38 +90,59 @@ __device__ __forceinline__ Item get_item(int it, const int2* __restrict__ work, 
   return x;
 }
 
-// One query row's online-softmax step over a 128-key score tile in TMEM (this
-// thread's lane): causal mask (keys > limit), running max in the exp2 domain,
-// P = 2^(s * scale - m) written back over the scores as bf16 pairs. The O
-// accumulator is rescaled (after PV of the previous tile landed, o_done of
-// global tile gt - 1) only when the max grows by more than 2^8; the final
-// 1 / l uses the same stale max, so the result is exact.
-__device__ __forceinline__ void softmax_tile(uint32_t ts, uint32_t to, int j, int limit, float scale_log2,
-                                             uint64_t* o_done, uint32_t gt, float& m, float& l) {
-  uint32_t v[4][32];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) tmem_ld32(ts + 32 * c, v[c]);
+// Two softmax threads share each query row (TMEM lane): warps 2-5 own score
+// / output columns 0-63 of their lane quarter, warps 6-9 columns 64-127.
+// Partial values are swapped through spare TMEM columns (384 + ...) of the
+// row's lane around a named barrier of the two warps.
+constexpr uint32_t kTmemXchg = 384;
+
+__device__ __forceinline__ float pair_exchange(uint32_t trow, uint32_t col_mine, uint32_t col_other, float v,
+                                               int bar_id) {
+  tmem_st1(trow + col_mine, __float_as_uint(v));
+  tmem_st_wait();
+  tc_fence_before();
+  named_bar_sync(bar_id, 64);
+  tc_fence_after();
+  const uint32_t o = tmem_ld1(trow + col_other);
   tmem_ld_wait();
-  const int k0 = j * kKeys;
-  // four independent max chains (one per 32-column chunk)
-  float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  if (k0 + kKeys - 1 > limit) {
+  return __uint_as_float(o);
+}
+
+// One half-row's online-softmax step over a 128-key score tile in TMEM:
+// causal mask (keys > limit), the row max from both halves (running, exp2
+// domain), P = 2^(s * scale - m) written back as bf16 pairs over the tile's
+// first 64 columns (keys 64h.. -> columns 32h..; the partner read its scores
+// before the exchange barrier). O (this half's 64 columns) is rescaled after
+// PV of the previous tile landed (o_done of global tile gt - 1) only when the
+// max grows by more than 2^8; the final 1 / l uses the same stale max, so the
+// result is exact. l is this half's partial sum.
+__device__ __forceinline__ void softmax_half(uint32_t trow, uint32_t ts, uint32_t to, int h, int j, int limit,
+                                             float scale_log2, uint64_t* o_done, uint32_t gt, int bar_id,
+                                             float& m, float& l) {
+  uint32_t v[2][32];
+  tmem_ld32(ts + 64 * h, v[0]);
+  tmem_ld32(ts + 64 * h + 32, v[1]);
+  tmem_ld_wait();
+  const int k0 = j * kKeys + 64 * h;
+  float mx2[2] = {-INFINITY, -INFINITY};
+  if (k0 + 63 > limit) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < 2; ++c)
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float sv = (k0 + 32 * c + i <= limit) ? __uint_as_float(v[c][i]) : -INFINITY;
         v[c][i] = __float_as_uint(sv);
-        mx4[c] = fmaxf(mx4[c], sv);
+        mx2[c] = fmaxf(mx2[c], sv);
       }
   } else {
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < 2; ++c)
 #pragma unroll
-      for (int i = 0; i < 32; ++i) mx4[c] = fmaxf(mx4[c], __uint_as_float(v[c][i]));
+      for (int i = 0; i < 32; ++i) mx2[c] = fmaxf(mx2[c], __uint_as_float(v[c][i]));
   }
-  const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-  const float mnew = mx * scale_log2;  // -inf stays -inf
+  const uint32_t xc = kTmemXchg + 2 * (gt & 1);
+  const float mine = fmaxf(mx2[0], mx2[1]);
+  const float mnew = fmaxf(mine, pair_exchange(trow, xc + h, xc + (h ^ 1), mine, bar_id)) * scale_log2;
   const bool resc = mnew > m + 8.f;
   const bool rescale_o = __any_sync(0xffffffffu, resc && j > 0);
   if (rescale_o) {
@@ -127,13 +150,13 @@ __device__ __forceinline__ void softmax_tile(uint32_t ts, uint32_t to, int j, in
     tc_fence_after();
     const float alpha = (resc && j > 0) ? ex2(m - mnew) : 1.f;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t o[32];
-      tmem_ld32(to + 32 * c, o);
+      tmem_ld32(to + 64 * h + 32 * c, o);
       tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-      tmem_st32(to + 32 * c, o);
+      tmem_st32(to + 64 * h + 32 * c, o);
     }
     tmem_st_wait();
   }
@@ -143,21 +166,15 @@ __device__ __forceinline__ void softmax_tile(uint32_t ts, uint32_t to, int j, in
   }
   const float mb = m == -INFINITY ? 0.f : m;
   float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  // P packed in place over the scores already consumed (column pair 2i, 2i+1
-  // of a 64-column half lands in word i of the half's first chunk)
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int e = 64 * c + 2 * i;
-      const float x0 = fmaf(__uint_as_float(v[e >> 5][e & 31]), scale_log2, -mb);
-      const float x1 = fmaf(__uint_as_float(v[(e + 1) >> 5][(e + 1) & 31]), scale_log2, -mb);
-      const float p0 = ex2(x0), p1 = ex2(x1);
-      ls[i & 7] += p0 + p1;
-      v[2 * c][i] = pack_bf16(p0, p1);
-    }
-    tmem_st32(ts + 32 * c, v[2 * c]);
+  for (int i = 0; i < 32; ++i) {
+    const int e = 2 * i;
+    const float p0 = ex2(fmaf(__uint_as_float(v[e >> 5][e & 31]), scale_log2, -mb));
+    const float p1 = ex2(fmaf(__uint_as_float(v[(e + 1) >> 5][(e + 1) & 31]), scale_log2, -mb));
+    ls[i & 7] += p0 + p1;
+    v[0][i] = pack_bf16(p0, p1);
   }
+  tmem_st32(ts + 32 * h, v[0]);
   l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
   // every PV completion is observed exactly once (here, in the rescale above,
   // or in the epilogue for the item's last tile): by the end of this tile's
@@ -165,12 +182,12 @@ __device__ __forceinline__ void softmax_tile(uint32_t ts, uint32_t to, int j, in
   if (j > 0 && !rescale_o) mbar_wait(o_done, (gt - 1) & 1);
 }
 
-// Epilogue of one query row: O / l from TMEM -> 128 bf16 (skipped for rows
-// past the item's tokens).
-__device__ __forceinline__ void store_rows(uint32_t to, bool valid, float l, __nv_bfloat16* dst) {
+// Epilogue of one half-row: O (this half's 64 dims) / l -> bf16 (skipped for
+// rows past the item's tokens).
+__device__ __forceinline__ void store_half(uint32_t to, bool valid, float l, __nv_bfloat16* dst) {
   const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < 2; ++c) {
     uint32_t o[32];
     tmem_ld32(to + 32 * c, o);
     tmem_ld_wait();
@@ -219,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[i], 256);
     }
     for (int i = 0; i < kKStages; ++i) {
       mbar_init(&k_full[i], 1);
@@ -230,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&v_empty[i], 1);
     }
     mbar_init(o_done, 1);
-    mbar_init(o_free, 128);
+    mbar_init(o_free, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -324,8 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   } else {
-    // ---------------- softmax + epilogue ----------------
+    // ---------------- softmax + epilogue: two threads per query row ----------------
     const int q = warp & 3;                 // TMEM lane quarter of this warp
+    const int h = (warp - 2) >> 2;          // column half of the row
+    const int bar_id = 1 + q;               // named barrier of the warp pair sharing these rows
     const int r = q * 32 + lane;            // query row within the item
     const uint32_t trow = tbase + (static_cast<uint32_t>(q * 32) << 16);
     uint32_t gt = 0;
@@ -339,16 +358,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b = gt & 1;
         mbar_wait(&s_full[b], (gt >> 1) & 1);
         tc_fence_after();
-        softmax_tile(trow + kTmemS + b * 128, trow + kTmemO, j, limit, g.scale_log2, o_done, gt, m, l);
+        softmax_half(trow, trow + kTmemS + b * 128, trow + kTmemO, h, j, limit, g.scale_log2, o_done, gt, bar_id,
+                     m, l);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[b]);
       }
-      // epilogue: O / l -> bf16 rows [token][head * 128]
+      // epilogue: O / (l_0 + l_1) -> bf16, this half's 64 dims of [token][head * 128]
       mbar_wait(o_done, (gt - 1) & 1);
       tc_fence_after();
-      store_rows(trow + kTmemO, valid, l,
-                 out + static_cast<size_t>(x.q_start + tk) * g.out_stride + (x.kvh * G + r % G) * kHD);
+      const float lt = l + pair_exchange(trow, kTmemXchg + 4 + h, kTmemXchg + 4 + (h ^ 1), l, bar_id);
+      store_half(trow + kTmemO + 64 * h, valid, lt,
+                 out + static_cast<size_t>(x.q_start + tk) * g.out_stride + (x.kvh * G + r % G) * kHD + 64 * h);
       tc_fence_before();
       mbar_arrive(o_free);
     }
