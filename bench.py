@@ -102,6 +102,9 @@ def parse():
                         "all-reduce kernels over NVLink, one engine, device clock); otherwise 1")
     p.add_argument("--tp-colocated", action="store_true",
                    help="place all TP ranks on one GPU (NX_TP_PEER_COLOCATED; a functional check of the TP path)")
+    p.add_argument("--token-budget", type=int, default=2048,
+                   help="ControllerConfig.token_budget (prefill tokens per batch; both engines) and chunk_size "
+                        "(monolithic chunk)")
     p.add_argument("--max-decode-batch", type=int, default=128,
                    help="ControllerConfig.max_decode_batch (reference default 64, domain.hpp:87)")
     return p.parse_args()
@@ -242,7 +245,7 @@ def load_calib(base):
 
 
 def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True, max_decode_batch=64,
-             alpha=1.3, beta=1.1, model="llama3-8b", gamma=None, static_r_p=50, tp=1):
+             alpha=1.3, beta=1.1, model="llama3-8b", gamma=None, static_r_p=50, tp=1, token_budget=2048):
     """tp > 1: the GpuSpec describes the TP group (peaks x tp; every GPU holds
     its kv heads of the same token pages, so the token capacity is one GPU's)."""
     m = nx.derive(*MODELS[model][0])
@@ -255,6 +258,7 @@ def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True,
             "monolithic": nx.NX_ENGINE_MONOLITHIC}[engine]
     ctrl = nx.lib().nx_controller_config_default()
     ctrl.max_decode_batch = max_decode_batch
+    ctrl.token_budget = ctrl.chunk_size = token_budget
     ctrl.alpha, ctrl.beta = alpha, beta
     if gamma is not None:
         ctrl.gamma = gamma
@@ -281,6 +285,7 @@ def reference_cfg(args, num_pages, page_tokens, engine=None):
     g.kv_capacity_bytes = (num_pages - 4096) * page_tokens * ref_kvbpt(args.model)
     ctrl, _, _ = reference.defaults()
     ctrl.max_decode_batch, ctrl.alpha, ctrl.beta = args.max_decode_batch, args.alpha, args.beta
+    ctrl.token_budget = ctrl.chunk_size = args.token_budget
     if args.gamma is not None:
         ctrl.gamma = args.gamma
     kind = {"nexus": _abi.NX_ENGINE_NEXUS, "static": _abi.NX_ENGINE_STATIC,
@@ -381,7 +386,7 @@ def main():
     num_pages = int(args.kv_gb * (1 << 30) * tp // (page_tokens * MODELS[args.model][1]))
     tp_mode = D.NX_TP_PEER_COLOCATED if args.tp_colocated else D.NX_TP_PEER
     dev = D.Device(D.arch_preset(args.model), num_pages=num_pages, page_tokens=page_tokens,
-                   max_prefill_tokens=2048 + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
+                   max_prefill_tokens=args.token_budget + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
                    green_contexts=not args.no_green and not (tp > 1 and args.tp_colocated),
                    seed=args.seed, device=0 if tp > 1 else local,
                    **(dict(tp_size=tp, tp_mode=tp_mode) if tp > 1 else {}))
@@ -390,7 +395,8 @@ def main():
 
     def cfg_for(engine):
         return make_cfg(nx, engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext,
-                        args.max_decode_batch, args.alpha, args.beta, args.model, args.gamma, args.static_r_p, tp)
+                        args.max_decode_batch, args.alpha, args.beta, args.model, args.gamma, args.static_r_p, tp,
+                        args.token_budget)
 
     cfg = cfg_for(args.engine)
     vocab = dev.arch.vocab
@@ -572,7 +578,8 @@ def main():
                    "calibration": os.path.basename(args.calib) if load_calib(args.calib) else "none",
                    "bw_ext": not args.no_bw_ext,
                    "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt},
-                   "max_decode_batch": args.max_decode_batch, "alpha": args.alpha, "beta": args.beta, "gamma": args.gamma,
+                   "max_decode_batch": args.max_decode_batch, "token_budget": args.token_budget,
+                   "alpha": args.alpha, "beta": args.beta, "gamma": args.gamma,
                    "kv_pool_gb": args.kv_gb,
                    "parallelism": (f"tp{tp}" + (" colocated on one GPU" if args.tp_colocated else " (peer-memory all-reduce)"))
                    if tp > 1 else f"replicas x{world}",

@@ -240,7 +240,7 @@ def fit_and_write(args, sweep, contention, total, pref, B, ctx):
         bw_sat[k] = b["bw_sat"]
     cf = fit_contention(contention)
     out = {
-        "model": args.model, "ref_model_preset": args.ref_model, "sm_count": total,
+        "model": args.model, "ref_model_preset": args.ref_model, "ref_dims": args.ref_dims, "sm_count": total,
         "gpu_spec": {"total_sm": total, "peak_compute": pf["peak_compute"], "peak_bandwidth": df["peak_bandwidth"]},
         "profile": {k: {"r_sat": getattr(prof, k).r_sat, "lambda": getattr(prof, k).lambda_} for k in OPS},
         "bw_sat": bw_sat, "contention": contention,

@@ -15,7 +15,8 @@ import paper_2507_06608_b200 as nx  # noqa: E402
 
 def main(base):
     cal = json.load(open(base + ".json"))
-    m = nx.model_preset(cal["ref_model_preset"])
+    m = (nx.derive(*[int(v) for v in cal["ref_dims"].split(",")]) if cal.get("ref_dims")
+         else nx.model_preset(cal["ref_model_preset"]))
     gs = cal["gpu_spec"]
     gpu = nx.gpu_spec(gs["total_sm"], gs["peak_compute"], gs["peak_bandwidth"], 150 << 30)
     prof, _ = nx.parse_kernel_profile(open(base + ".calib").read())
