@@ -79,6 +79,9 @@ def parse():
     p.add_argument("--compare", default="monolithic",
                    help="comma list of same-kernel baseline engines (monolithic, static) run on the identical "
                         "traces and prompts after the timed region; 'none' to skip")
+    p.add_argument("--compare-steps", type=int, default=6,
+                   help="baseline arm runs the first min(steps, this) timed traces (bounds the bench's wall "
+                        "time); the ratios compare this engine on the same traces")
     p.add_argument("--no-green", action="store_true")
     p.add_argument("--calib", default=None,
                    help="calibration base path (.calib + .json from paper_2507_06608_b200.calibrate); "
@@ -493,12 +496,15 @@ def main():
     # Same-kernel baselines (BASELINE.md §2 / SURVEY §8(f)1): the identical traces
     # and prompt buffers served by the monolithic chunked-prefill engine (and/or
     # a static split), after the timed region so `value` times this engine only.
-    mine = summarize(results)
+    n_cmp = max(1, min(args.steps, args.compare_steps))
+    mine = summarize(results[:n_cmp])
     baselines = {}
     for bname in [e.strip() for e in args.compare.split(",")]:
         if not bname or bname == "none" or bname == args.engine:
             continue
-        b = summarize([one_step(args.warmup + s, cfg_for(bname)) for s in range(args.steps)])
+        b = summarize([one_step(args.warmup + s, cfg_for(bname)) for s in range(n_cmp)])
+        b["traces"] = f"the first {n_cmp} timed traces"
+        b["this_engine_same_traces"] = mine
         b["this_engine_over_baseline"] = {
             "goodput": mine["goodput"] / b["goodput"] if b["goodput"] else None,
             "goodput_makespan": mine["goodput_makespan"] / b["goodput_makespan"] if b["goodput_makespan"] else None,
