@@ -103,6 +103,10 @@ def parse():
                    help="tensor-parallel group size (C4). 0 = auto: under torchrun with --model llama3-70b the "
                         "whole job is one TP group of WORLD_SIZE GPUs driven by rank 0 (NX_TP_PEER: our peer-memory "
                         "all-reduce kernels over NVLink, one engine, device clock); otherwise 1")
+    p.add_argument("--tp-mode", default="peer", choices=["peer", "nccl"],
+                   help="peer: rank 0 drives every GPU of the group (our peer-memory collectives); nccl: one "
+                        "process per GPU with NCCL all-reduces, rank 0's engine forwarding every launch to the "
+                        "followers (device.tp_follow) so all ranks run identical batches on its device clock")
     p.add_argument("--tp-colocated", action="store_true",
                    help="place all TP ranks on one GPU (NX_TP_PEER_COLOCATED; a functional check of the TP path)")
     p.add_argument("--token-budget", type=int, default=2048,
@@ -372,7 +376,10 @@ def main():
         run_reference(args, rank, world, dist)
         return
     tp = args.tp or (world if args.model == "llama3-70b" and world > 1 else 1)
-    if tp > 1 and world > 1:
+    tp_nccl = tp > 1 and args.tp_mode == "nccl"
+    if tp_nccl and tp != world:
+        raise SystemExit(f"--tp-mode nccl needs one process per rank: --tp {tp} != WORLD_SIZE {world}")
+    if tp > 1 and world > 1 and not tp_nccl:
         # one TP group over all GPUs of the job, driven by rank 0 (one engine,
         # one device clock); the other ranks only hold the barriers
         if tp != world:
@@ -387,12 +394,36 @@ def main():
 
     page_tokens = 16
     num_pages = int(args.kv_gb * (1 << 30) * tp // (page_tokens * MODELS[args.model][1]))
-    tp_mode = D.NX_TP_PEER_COLOCATED if args.tp_colocated else D.NX_TP_PEER
-    dev = D.Device(D.arch_preset(args.model), num_pages=num_pages, page_tokens=page_tokens,
-                   max_prefill_tokens=args.token_budget + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
-                   green_contexts=not args.no_green and not (tp > 1 and args.tp_colocated),
-                   seed=args.seed, device=0 if tp > 1 else local,
-                   **(dict(tp_size=tp, tp_mode=tp_mode) if tp > 1 else {}))
+    dev_kw = dict(num_pages=num_pages, page_tokens=page_tokens,
+                  max_prefill_tokens=args.token_budget + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
+                  seed=args.seed)
+    if tp_nccl:
+        # one communicator per lane; ids from rank 0, every rank holds its shard
+        box = [[D.nccl_unique_id(), D.nccl_unique_id()] if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        dev = D.Device(D.arch_preset(args.model), green_contexts=not args.no_green, device=local, tp_size=tp,
+                       tp_rank=rank, tp_mode=D.NX_TP_NCCL, nccl_ids=box[0], **dev_kw)
+        if rank != 0:
+            def recv():
+                b = [None]
+                dist.broadcast_object_list(b, src=0)
+                return b[0]
+            D.tp_follow(dev, recv)
+            dev.close()
+            return
+    else:
+        tp_mode = D.NX_TP_PEER_COLOCATED if args.tp_colocated else D.NX_TP_PEER
+        dev = D.Device(D.arch_preset(args.model), green_contexts=not args.no_green and not (tp > 1 and args.tp_colocated),
+                       device=0 if tp > 1 else local, **(dict(tp_size=tp, tp_mode=tp_mode) if tp > 1 else {}),
+                       **dev_kw)
+    try:
+        run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_pages, page_tokens)
+    finally:
+        if tp_nccl:
+            dist.broadcast_object_list([None], src=0)  # followers leave tp_follow
+
+
+def run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_pages, page_tokens):
     dev.set_profiling(args.profile_every)
     group_world = 1 if tp > 1 else world  # ranks whose results are aggregated
 
@@ -418,6 +449,8 @@ def main():
         trace, prompts = step_inputs(step)
         t0 = time.perf_counter()
         eng = nx.Engine(scfg or cfg, device=dev)
+        if tp_nccl:
+            eng.set_launch_observer(lambda b: dist.broadcast_object_list([b], src=0))
         eng.set_slo(args.slo_ttft, args.slo_tbt)
         eng.set_logging(True, False)
         for t, p in zip(trace, prompts):
@@ -449,7 +482,7 @@ def main():
     dev.reset_kernel_stats()
     k0 = dev.kernel_stats().kernel_launches
     clocks = ClockSampler(local)
-    if dist:
+    if dist and not tp_nccl:  # (NCCL followers are inside tp_follow, in lockstep through the collectives)
         dist.barrier()
     clocks.start()
     results = [one_step(args.warmup + s) for s in range(args.steps)]
@@ -460,7 +493,7 @@ def main():
     span = sum(r["makespan"] for r in results)
     window = sum(r["window"] for r in results)
     wall = sum(r["wall"] for r in results)
-    if dist and tp > 1:
+    if dist and tp > 1 and not tp_nccl:
         dist.barrier()
     if dist and tp == 1:
         import torch
@@ -587,7 +620,9 @@ def main():
                    "max_decode_batch": args.max_decode_batch, "token_budget": args.token_budget,
                    "alpha": args.alpha, "beta": args.beta, "gamma": args.gamma,
                    "kv_pool_gb": args.kv_gb,
-                   "parallelism": (f"tp{tp}" + (" colocated on one GPU" if args.tp_colocated else " (peer-memory all-reduce)"))
+                   "parallelism": (f"tp{tp}" + (" colocated on one GPU" if args.tp_colocated
+                                                else " (NCCL all-reduce, one process per GPU)" if tp_nccl
+                                                else " (peer-memory all-reduce)"))
                    if tp > 1 else f"replicas x{world}",
                    "l2": "inputs > L2 (16 GB weights streamed per decode step)"},
         "ttft_p50": nearest_rank(ttft, 50), "ttft_p99": nearest_rank(ttft, 99),

@@ -568,6 +568,17 @@ int nx_device_launch(nx_device* dev, const nx_batch_desc* b);
 int nx_device_wait(nx_device* dev, int32_t lane, int32_t* sampled, float* logits,
                    double* device_ms);
 
+/* Launch observer (new): called on every engine launch, before the bound
+ * device (if any) sees it, with the batch in nx_batch_desc form (tokens NULL
+ * when the engine holds no token ids, i.e. no device bound). The pointers are
+ * valid during the call only. Under NX_TP_NCCL the ranks' devices must run
+ * identical batches in identical per-lane order: rank 0's engine serves on
+ * the device clock and its observer forwards each batch to the followers,
+ * which replay it with nx_device_launch (paper_2507_06608_b200.device
+ * tp_follow). */
+typedef void (*nx_launch_observer)(void* user, const nx_batch_desc* batch);
+int nx_engine_set_launch_observer(nx_engine* eng, nx_launch_observer fn, void* user);
+
 /* Kernel-class timing (CUDA events on the launching stream, every
  * `sample_every`-th batch per lane; 0 disables) with algorithmic work. */
 #define NX_K_GEMM_DECODE 0  /* projections on the decode lane (HBM-bound weight stream) */

@@ -343,6 +343,26 @@ class SimResult:
     sim_end_s: float = 0.0
 
 
+_LAUNCH_OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
+def batch_from_desc(ptr) -> dict:
+    """An nx_batch_desc (the device ABI's batch) as dict(lane, sm_pct,
+    members=[dict(tokens, n, start, pages, sample)]); n is the member's token
+    count, tokens are [] when the engine holds no token ids (no device bound)."""
+    from ._dev_abi import BatchDesc
+    d = C.cast(ptr, C.POINTER(BatchDesc)).contents
+    members, t0, p0 = [], 0, 0
+    for i in range(d.n_members):
+        n, npg = d.n_tokens[i], d.n_pages[i]
+        toks = [d.tokens[t0 + k] for k in range(n)] if d.tokens else []
+        members.append(dict(tokens=toks, n=int(n), start=int(d.start_pos[i]),
+                            pages=[d.pages[p0 + k] for k in range(npg)], sample=bool(d.sample[i])))
+        t0 += n
+        p0 += npg
+    return dict(lane=int(d.lane), sm_pct=int(d.sm_pct), members=members)
+
+
 class Engine:
     """The step executor (nx_engine_*): submit / step / run / logs / KV."""
 
@@ -378,10 +398,13 @@ class Engine:
         self._call(lib().nx_submit_trace(self._h, arr, len(trace)))
 
     def step(self) -> int:
-        return self._call(lib().nx_step(self._h))
+        rc = self._call(lib().nx_step(self._h))
+        self._raise_observer_error()
+        return rc
 
     def run(self) -> None:
         self._call(lib().nx_run(self._h))
+        self._raise_observer_error()
 
     def set_replay_latencies(self, lat: Sequence[float]) -> None:
         arr = (C.c_double * max(1, len(lat)))(*lat)
@@ -392,6 +415,32 @@ class Engine:
 
     def set_slo(self, ttft_s: float, tbt_s: float) -> None:
         lib().nx_engine_set_slo(self._h, ttft_s, tbt_s)
+
+    def set_launch_observer(self, fn: Callable[[dict], None] | None) -> None:
+        """fn(batch) on every launch, before the device runs it (batch_from_desc
+        form): rank 0 of an NX_TP_NCCL group forwards its batches to the
+        followers with it (device.tp_follow). Exceptions inside fn cannot
+        cross the C boundary; they are stored and re-raised by run()/step()."""
+        if fn is None:
+            self._obs = None
+            _check(lib().nx_engine_set_launch_observer(self._h, None, None))
+            return
+
+        def cb(_user, ptr):
+            try:
+                fn(batch_from_desc(ptr))
+            except BaseException as e:  # noqa: BLE001 -- surfaced after the C call returns
+                self._obs_error = e
+
+        self._obs_error = None
+        self._obs = _LAUNCH_OBSERVER(cb)
+        _check(lib().nx_engine_set_launch_observer(self._h, self._obs, None))
+
+    def _raise_observer_error(self) -> None:
+        e = getattr(self, "_obs_error", None)
+        if e is not None:
+            self._obs_error = None
+            raise RuntimeError("launch observer failed") from e
 
     def configure_pages(self, page_tokens: int, num_pages: int) -> None:
         _check(lib().nx_kv_configure(self._h, page_tokens, num_pages))

@@ -203,6 +203,7 @@ _PROTOS = {
     "nx_engine_set_replay_latencies": (C.c_int, [C.c_void_p, P(C.c_double), sz]),
     "nx_engine_set_logging": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     "nx_engine_set_slo": (C.c_int, [C.c_void_p, C.c_double, C.c_double]),
+    "nx_engine_set_launch_observer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "nx_engine_get_stats": (C.c_int, [C.c_void_p, P(EngineStats)]),
     "nx_engine_event_log": (C.c_int, [C.c_void_p, C.c_char_p, sz, P(sz)]),
     "nx_engine_decision_log": (C.c_int, [C.c_void_p, C.c_char_p, sz, P(sz)]),

@@ -399,6 +399,11 @@ int nx_engine_set_slo(nx_engine* eng, double ttft_s, double tbt_s) {
   return NX_OK;
 }
 
+int nx_engine_set_launch_observer(nx_engine* eng, nx_launch_observer fn, void* user) {
+  eng->e.set_launch_observer(fn, user);
+  return NX_OK;
+}
+
 int nx_engine_get_stats(const nx_engine* eng, nx_engine_stats* out) {
   *out = eng->e.stats();
   return NX_OK;

@@ -262,6 +262,7 @@ void Engine::begin(Lane& lane, int slot, int lane_kind, double predicted) {
     if (!pages_.ensure(m.id, live(m.id).rec.prefilled + m.tokens, nullptr))
       throw RuntimeErr("KV page pool exhausted");
   }
+  if (obs_) notify_observer(lane, slot, lane_kind);
   if (exec_) dispatch_device(lane, slot, lane_kind);
   std::vector<EvMember> ev;
   for (const auto& m : lane.dec) ev.push_back({m.id, m.tokens, 0});
@@ -274,19 +275,58 @@ void Engine::begin(Lane& lane, int slot, int lane_kind, double predicted) {
   ++launches_;
 }
 
+// The SM share a launch runs on. Device layout only (the decision log keeps
+// the controller's r_p): a decode batch launched while the prefill lane is
+// idle and no prompt waits runs on the whole GPU instead of leaving the
+// prefill SMs dark. A prefill batch launched before it finishes is ordered
+// after it by the executor (Model::launch), so the two never share SMs.
+int Engine::device_share(const Lane& lane, int lane_kind) const {
+  if (lane_kind == NX_LANE_MIXED) return 100;
+  if (lane_kind == NX_LANE_PREFILL) return lane.r_p;
+  if (decode_full_when_idle_ && !prefill_.busy && prefill_queue().empty()) return 100;
+  return 100 - lane.r_p;
+}
+
+// nx_batch_desc of a launch (members in log order: decode first, then prefill
+// chunks) for the launch observer.
+void Engine::notify_observer(const Lane& lane, int slot, int lane_kind) const {
+  std::vector<int32_t> ntok, sample, toks, npg, pages;
+  std::vector<int64_t> start;
+  auto add = [&](uint64_t id, int32_t n, int64_t s0, int32_t smp) {
+    const Live& l = live(id);
+    ntok.push_back(n);
+    start.push_back(s0);
+    sample.push_back(smp);
+    if (!l.tokens.empty()) toks.insert(toks.end(), l.tokens.begin() + s0, l.tokens.begin() + s0 + n);
+    const std::vector<int32_t>* pt = pages_.table(id);
+    npg.push_back(pt ? static_cast<int32_t>(pt->size()) : 0);
+    if (pt) pages.insert(pages.end(), pt->begin(), pt->end());
+  };
+  for (const auto& m : lane.dec) {
+    const Live& l = live(m.id);
+    add(m.id, 1, l.rec.prompt + l.rec.decoded - 1, 1);
+  }
+  for (const auto& m : lane.pre) {
+    const Live& l = live(m.id);
+    add(m.id, static_cast<int32_t>(m.tokens), l.rec.prefilled, l.rec.prefilled + m.tokens == l.rec.prompt ? 1 : 0);
+  }
+  nx_batch_desc d{};
+  d.lane = slot;
+  d.sm_pct = device_share(lane, lane_kind);
+  d.n_members = static_cast<int32_t>(ntok.size());
+  d.n_tokens = ntok.data();
+  d.start_pos = start.data();
+  d.sample = sample.data();
+  d.tokens = toks.size() == 0 ? nullptr : toks.data();
+  d.n_pages = npg.data();
+  d.pages = pages.data();
+  obs_(obs_user_, &d);
+}
+
 void Engine::dispatch_device(Lane& lane, int slot, int lane_kind) {
   ExecBatch b;
   b.lane_kind = lane_kind;
-  b.sm_pct = lane_kind == NX_LANE_MIXED ? 100
-             : lane_kind == NX_LANE_PREFILL ? lane.r_p
-                                            : 100 - lane.r_p;
-  // Device layout only (the decision log keeps the controller's r_p): a
-  // decode batch launched while the prefill lane is idle and no prompt waits
-  // runs on the whole GPU instead of leaving the prefill SMs dark. A prefill
-  // batch launched before it finishes is ordered after it by the executor
-  // (Model::launch), so the two never share SMs.
-  if (lane_kind == NX_LANE_DECODE && decode_full_when_idle_ && !prefill_.busy && prefill_queue().empty())
-    b.sm_pct = 100;
+  b.sm_pct = device_share(lane, lane_kind);
   for (const auto& m : lane.dec) {
     const Live& l = live(m.id);
     const std::vector<int32_t>* pt = pages_.table(m.id);

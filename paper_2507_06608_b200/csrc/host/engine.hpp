@@ -65,6 +65,13 @@ class Engine {
     slo_tbt_ = tbt;
   }
   void set_prompt_seed(uint64_t s) { prompt_seed_ = s; }
+  // Called on every launch, before the device sees it, with the batch as the
+  // device ABI describes it (TP followers replay rank 0's launches from it).
+  using LaunchObserver = void (*)(void* user, const nx_batch_desc* batch);
+  void set_launch_observer(LaunchObserver fn, void* user) {
+    obs_ = fn;
+    obs_user_ = user;
+  }
 
   // Introspection.
   std::string event_log() const;
@@ -129,6 +136,8 @@ class Engine {
   }
   double now_s() const;
   void dispatch_device(Lane& lane, int slot, int lane_kind);
+  int device_share(const Lane& lane, int lane_kind) const;
+  void notify_observer(const Lane& lane, int slot, int lane_kind) const;
 
   nx_sim_config cfg_;
   bool dynamic_, monolithic_;
@@ -159,6 +168,8 @@ class Engine {
   std::chrono::steady_clock::time_point t0_;
   double slo_ttft_ = 1.0, slo_tbt_ = 0.05;
   uint64_t prompt_seed_ = 1;
+  LaunchObserver obs_ = nullptr;
+  void* obs_user_ = nullptr;
 };
 
 }  // namespace nxb

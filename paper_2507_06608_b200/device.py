@@ -99,6 +99,31 @@ def shard_plan(a: Arch, tp_size: int, rank: int) -> TpShard:
     return s
 
 
+def tp_follow(dev, recv) -> int:
+    """Follower loop of an NX_TP_NCCL group served on rank 0's device clock.
+
+    Rank 0's engine forwards every launch (Engine.set_launch_observer) and
+    this loop replays it on the follower's shard: `recv()` returns the next
+    batch (the batch_from_desc dict) or None at the end. A lane's next batch
+    is launched after that lane's previous one finished, exactly as on rank
+    0, so every rank issues the same batches in the same per-lane order and
+    the per-lane NCCL collectives pair up. Returns the number of launches."""
+    pending, n = set(), 0
+    while True:
+        b = recv()
+        if b is None:
+            break
+        lane = b["lane"]
+        if lane in pending:
+            dev.wait(lane)
+        dev.launch(b["members"], lane=lane, sm_pct=b["sm_pct"])
+        pending.add(lane)
+        n += 1
+    for lane in sorted(pending):
+        dev.wait(lane)
+    return n
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib().nx_nccl_unique_id(buf))

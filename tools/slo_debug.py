@@ -14,10 +14,12 @@ from paper_2507_06608_b200 import device as D  # noqa: E402
 ENGINE = os.environ.get("ENGINE", "nexus")
 RATE = float(os.environ.get("RATE", "96"))
 N = int(os.environ.get("N", "2000"))
+MDB = int(os.environ.get("MDB", "128"))
+BETA = float(os.environ.get("BETA", "2.0"))
 calib = os.path.join(REPO, "profiles", "b200_llama3_8b")
 num_pages = int(80.0 * (1 << 30) // (16 * bench.MODELS["llama3-8b"][1]))
-dev = D.Device(D.arch_preset("llama3-8b"), num_pages=num_pages, max_prefill_tokens=2048 + 128, max_decode_batch=128)
-cfg = bench.make_cfg(nx, ENGINE, num_pages, 16, nx.NX_CLOCK_DEVICE, calib, True, 128, 1.3, 2.0, "llama3-8b", 5000.0)
+dev = D.Device(D.arch_preset("llama3-8b"), num_pages=num_pages, max_prefill_tokens=2048 + MDB, max_decode_batch=MDB)
+cfg = bench.make_cfg(nx, ENGINE, num_pages, 16, nx.NX_CLOCK_DEVICE, calib, True, MDB, 1.3, BETA, "llama3-8b", 5000.0)
 trace = nx.workload_trace("sharegpt", RATE, N, 201)
 rng = np.random.default_rng(201)
 eng = nx.Engine(cfg, device=dev)
@@ -52,6 +54,17 @@ for rid, ts in times.items():
             big = [round(g * 1e3, 1) for g in gaps[-5:]]
             print("miss", rid, "tokens", len(ts), "ttft", round(tt, 3), "largest gaps ms", big)
 print("requests", len(times), "miss_ttft", miss_ttft, "miss_tbt", miss_tbt, "miss by output length bucket", sorted(hist.items()))
+# decode launches: batch size, applied share, latency
+dl = []
+for line in eng.event_log().splitlines():
+    c = line.split("\t")
+    if c[2] == "launch" and c[1] == "decode":
+        dl.append((len(c[3].split(",")), int(c[4]), float(c[6])))
+if dl:
+    big = sorted(dl, key=lambda x: -x[2])[:5]
+    print("decode launches", len(dl), "mean rows", round(sum(x[0] for x in dl) / len(dl), 1),
+          "mean ms", round(1e3 * sum(x[2] for x in dl) / len(dl), 2), "slowest (rows, r_p, ms)",
+          [(a, b, round(1e3 * c, 1)) for a, b, c in big])
 
 # prefill-lane composition: tokens per prefill (or mixed) batch, its latency, lane busy time
 sizes, lats, dec_rows, busy = [], [], [], 0.0
