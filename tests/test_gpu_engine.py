@@ -110,3 +110,53 @@ def test_static_and_monolithic_engines_on_device(nx, tiny_dev):
             assert eng.event_log() == reference.run(cfg, trace)["event_log"]
         for q in eng.requests():
             assert len(eng.tokens(q.id)) == q.prompt_len + q.output_len
+
+
+def test_launch_observer_replays_on_a_second_device(nx, tiny_dev):
+    """The NX_TP_NCCL leader / follower protocol on one GPU: rank 0's engine
+    forwards every launch (with the token ids it holds once a device is bound)
+    and a second device with the same weights replays them with
+    device.tp_follow; every token the follower samples is the token the
+    engine appended for that member."""
+    from paper_2507_06608_b200 import device as D
+    tiny = nx.derive(256, 1024, 2, 4, 2)
+    trace = nx.workload_trace("sharegpt", 50.0, 24, 9)
+    cfg = nx.sim_config(tiny, nx.gpu_preset("desk"))
+    eng = nx.Engine(cfg, device=tiny_dev)
+    sent = []
+    eng.set_launch_observer(sent.append)
+    eng.submit_trace(trace)
+    eng.run()
+    launches = [l.split("\t") for l in eng.event_log().splitlines() if l.split("\t")[2] == "launch"]
+    assert len(sent) == len(launches) > 10
+    follower = D.Device(D.arch_preset("tiny"), num_pages=tiny_dev.cfg.num_pages, seed=5)
+    try:
+        fifo, produced = {}, {}
+        launch0, wait0 = follower.launch, follower.wait
+        order = []
+
+        def launch_tracked(members, lane=0, sm_pct=100):
+            order.append(lane)
+            fifo.setdefault(lane, []).append(len(order) - 1)
+            launch0(members, lane=lane, sm_pct=sm_pct)
+
+        def wait(lane):
+            toks, ms = wait0(lane)
+            produced[fifo[lane].pop(0)] = toks
+            return toks, ms
+
+        follower.launch, follower.wait = launch_tracked, wait
+        it = iter(sent + [None])
+        assert D.tp_follow(follower, lambda: next(it)) == len(sent)
+        checked = 0
+        for k, (b, l) in enumerate(zip(sent, launches)):
+            ids = [int(m.split(":")[0]) for m in l[3].split(",")]
+            toks = iter(produced[k])
+            for rid, m in zip(ids, b["members"]):
+                assert len(m["tokens"]) == m["n"]
+                if m["sample"]:
+                    assert next(toks) == eng.tokens(rid)[m["start"] + m["n"]]
+                    checked += 1
+        assert checked > 50
+    finally:
+        follower.close()
