@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--beta", type=float, default=2.0)
     ap.add_argument("--gamma", type=float, default=5000.0)
     ap.add_argument("--max-decode-batch", type=int, default=128)
+    ap.add_argument("--token-budget", type=int, default=2048, help="prefill tokens per batch (both engines)")
     ap.add_argument("--kv-gb", type=float, default=80.0)
     ap.add_argument("--slo-ttft", type=float, default=1.0)
     ap.add_argument("--slo-tbt", type=float, default=0.05)
@@ -50,7 +51,7 @@ def main():
     page = 16
     num_pages = int(args.kv_gb * (1 << 30) // (page * bench.MODELS[args.model][1]))
     dev = D.Device(D.arch_preset(args.model), num_pages=num_pages, page_tokens=page,
-                   max_prefill_tokens=2048 + args.max_decode_batch, max_decode_batch=args.max_decode_batch)
+                   max_prefill_tokens=args.token_budget + args.max_decode_batch, max_decode_batch=args.max_decode_batch)
     vocab = dev.arch.vocab
     seeds = [int(x) for x in args.seeds.split(",")]
     probes = open(args.out + ".jsonl", "a")
@@ -60,7 +61,7 @@ def main():
         if name.startswith("static"):
             kind, share = "static", int(name[6:] or 50)
         return bench.make_cfg(nx, kind, num_pages, page, nx.NX_CLOCK_DEVICE, calib, True, args.max_decode_batch,
-                              1.3, args.beta, args.model, args.gamma, share)
+                              1.3, args.beta, args.model, args.gamma, share, 1, args.token_budget)
 
     def probe(name, rate):
         cfg = engine_cfg(name)
@@ -110,7 +111,8 @@ def main():
     summary["config"] = {"model": args.model, "workload": args.workload, "requests_per_seed": args.requests,
                          "seeds": seeds, "target_attainment": args.target,
                          "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt}, "beta": args.beta,
-                         "gamma": args.gamma, "max_decode_batch": args.max_decode_batch}
+                         "gamma": args.gamma, "max_decode_batch": args.max_decode_batch,
+                         "token_budget": args.token_budget}
     json.dump(summary, open(args.out + ".json", "w"), indent=1)
     print(json.dumps(summary))
 
