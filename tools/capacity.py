@@ -27,6 +27,22 @@ import paper_2507_06608_b200 as nx  # noqa: E402
 from paper_2507_06608_b200 import device as D  # noqa: E402
 
 
+def bisect_capacity(attainment_at, lo, hi, tol, target):
+    """Highest rate in [lo, hi] whose attainment meets `target`, to within
+    `tol` (attainment assumed non-increasing in the rate)."""
+    if attainment_at(lo) < target:
+        return {"capacity_rps": None, "note": f"below target at {lo}"}
+    if hi <= lo or attainment_at(hi) >= target:
+        return {"capacity_rps": hi, "note": "target met at the upper bound"}
+    while hi - lo > tol:
+        mid = 0.5 * (lo + hi)
+        if attainment_at(mid) >= target:
+            lo = mid
+        else:
+            hi = mid
+    return {"capacity_rps": lo, "first_failing_rps": hi}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama3-8b")
@@ -94,20 +110,7 @@ def main():
 
     summary = {}
     for name in args.engines.split(","):
-        lo, hi = args.lo, args.hi
-        if probe(name, lo) < args.target:
-            summary[name] = {"capacity_rps": None, "note": f"below target at {lo}"}
-            continue
-        if probe(name, hi) >= args.target:
-            summary[name] = {"capacity_rps": hi, "note": "target met at the upper bound"}
-            continue
-        while hi - lo > args.tol:
-            mid = 0.5 * (lo + hi)
-            if probe(name, mid) >= args.target:
-                lo = mid
-            else:
-                hi = mid
-        summary[name] = {"capacity_rps": lo, "first_failing_rps": hi}
+        summary[name] = bisect_capacity(lambda rate: probe(name, rate), args.lo, args.hi, args.tol, args.target)
     summary["config"] = {"model": args.model, "workload": args.workload, "requests_per_seed": args.requests,
                          "seeds": seeds, "target_attainment": args.target,
                          "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt}, "beta": args.beta,
