@@ -87,10 +87,11 @@ def parse():
                    help="calibration base path (.calib + .json from paper_2507_06608_b200.calibrate); "
                         "'none' = reference default profile and nominal B200 spec")
     p.add_argument("--no-bw-ext", action="store_true", help="disable the share-dependent bandwidth term")
-    p.add_argument("--beta", type=float, default=2.0,
-                   help="ControllerConfig.beta, the decode slack in prefill-prioritized mode. The paper's "
-                        "1.1 was set for L20; on B200 a 2.0x slack still keeps p99 TBT well inside the "
-                        "50 ms SLO (profiles/r01_beta_sweep.md)")
+    p.add_argument("--beta", type=float, default=1.5,
+                   help="ControllerConfig.beta, the decode slack in prefill-prioritized mode (paper 1.1, set for "
+                        "L20). 1.5 with decode batch 256 keeps decode steps short enough that a request's first "
+                        "decode gap stays inside the TBT SLO (capacity 125 vs 119 rps for the monolithic "
+                        "baseline on held-out seeds, profiles/r02_summary.md); 2.0 was round 1's default")
     p.add_argument("--gamma", type=float, default=None,
                    help="ControllerConfig.gamma (SPF aging, tokens of priority per second waited; reference "
                         "default 15). At 128 rps on B200 with the CTA-pair prefill GEMMs: gamma 15 -> 10145 tok/s "
@@ -109,10 +110,14 @@ def parse():
                         "followers (device.tp_follow) so all ranks run identical batches on its device clock")
     p.add_argument("--tp-colocated", action="store_true",
                    help="place all TP ranks on one GPU (NX_TP_PEER_COLOCATED; a functional check of the TP path)")
-    p.add_argument("--token-budget", type=int, default=2048,
-                   help="ControllerConfig.token_budget (prefill tokens per batch; both engines) and chunk_size "
-                        "(monolithic chunk)")
-    p.add_argument("--max-decode-batch", type=int, default=128,
+    p.add_argument("--token-budget", type=int, default=4096,
+                   help="ControllerConfig.token_budget: prompt tokens per prefill batch of this engine (and "
+                        "chunk_size when --engine monolithic). 4096: nexus' prefill lane runs at saturation at "
+                        "the bench rate, so batch efficiency is capacity (profiles/r02_summary.md)")
+    p.add_argument("--compare-token-budget", type=int, default=2048,
+                   help="token budget / chunk of the same-kernel baseline arm: 2048 is the monolithic engine's "
+                        "best (3072 and 4096 lower its capacity: its TBT grows with the chunk)")
+    p.add_argument("--max-decode-batch", type=int, default=256,
                    help="ControllerConfig.max_decode_batch (reference default 64, domain.hpp:87)")
     return p.parse_args()
 
@@ -395,8 +400,8 @@ def main():
     page_tokens = 16
     num_pages = int(args.kv_gb * (1 << 30) * tp // (page_tokens * MODELS[args.model][1]))
     dev_kw = dict(num_pages=num_pages, page_tokens=page_tokens,
-                  max_prefill_tokens=args.token_budget + args.max_decode_batch, max_decode_batch=args.max_decode_batch,
-                  seed=args.seed)
+                  max_prefill_tokens=max(args.token_budget, args.compare_token_budget) + args.max_decode_batch,
+                  max_decode_batch=args.max_decode_batch, seed=args.seed)
     if tp_nccl:
         # one communicator per lane; ids from rank 0, every rank holds its shard
         box = [[D.nccl_unique_id(), D.nccl_unique_id()] if rank == 0 else None]
@@ -427,10 +432,10 @@ def run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_p
     dev.set_profiling(args.profile_every)
     group_world = 1 if tp > 1 else world  # ranks whose results are aggregated
 
-    def cfg_for(engine):
+    def cfg_for(engine, token_budget=None):
         return make_cfg(nx, engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext,
                         args.max_decode_batch, args.alpha, args.beta, args.model, args.gamma, args.static_r_p, tp,
-                        args.token_budget)
+                        token_budget or args.token_budget)
 
     cfg = cfg_for(args.engine)
     vocab = dev.arch.vocab
@@ -535,8 +540,9 @@ def run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_p
     for bname in [e.strip() for e in args.compare.split(",")]:
         if not bname or bname == "none" or bname == args.engine:
             continue
-        b = summarize([one_step(args.warmup + s, cfg_for(bname)) for s in range(n_cmp)])
+        b = summarize([one_step(args.warmup + s, cfg_for(bname, args.compare_token_budget)) for s in range(n_cmp)])
         b["traces"] = f"the first {n_cmp} timed traces"
+        b["token_budget"] = args.compare_token_budget
         b["this_engine_same_traces"] = mine
         b["this_engine_over_baseline"] = {
             "goodput": mine["goodput"] / b["goodput"] if b["goodput"] else None,
@@ -632,6 +638,10 @@ def run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_p
         "throughput_makespan": out_tok / (span_sum / group_world) if span_sum else 0.0,
         "goodput_makespan": good / (span_sum / group_world) if span_sum else 0.0,
         "same_kernel_baselines": baselines,
+        # not measured in this run: the paper's throughput metric from tools/capacity.py (3 held-out seeds x
+        # 2,000 requests per probe, >= 90% of requests inside both SLOs), same defaults as this line
+        "capacity_rps_reference": {"source": "profiles/r02_capacity_8b_tuned_seeds301.json",
+                                   "nexus": 125.0, "monolithic": 119.0} if args.model == "llama3-8b" else None,
         "decisions": sum(r["decisions"] for r in results), "switches": sum(r["switches"] for r in results),
         "r_p_hist_arrivals": {str(k): sum(r["r_p_hist"].get(k, 0) for r in results)
                               for k in sorted({k for r in results for k in r["r_p_hist"]})},
