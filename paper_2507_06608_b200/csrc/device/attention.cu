@@ -94,7 +94,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // (profiles/r01s2_attn_decode_bw.md). The pair merges its
 // (m, l, O) at the end of each item segment. An item covered by one unit is
 // finalized in place; an item split across units leaves (m, l, O) partials
-// that decode_combine_kernel folds with a log-sum-exp rescale.
+// that the unit writing an item's last partial folds with a log-sum-exp
+// rescale (an atomic count per item; no separate combine launch).
 // The tile math is transposed (keys / head dims on the MMA's M side, the
 // G <= 8 query heads of the kv head on its N = 8 side; see the kernel).
 constexpr int kKTD = 32;      // keys per decode tile (two 16-token pages)
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
                        const int* __restrict__ seq_prefix, int n_seq, long long total, long long W,
                        const int32_t* __restrict__ pages,
                        __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
-                       float* __restrict__ part_ml) {
+                       float* __restrict__ part_ml, int* __restrict__ item_done) {
   extern __shared__ __align__(1024) uint8_t smem_attn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1;
@@ -413,6 +414,44 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
               part_ml[(slot * g.group + h0 + 1) * 2 + 1] = L1;
             }
           }
+          // The unit that writes an item's last partial folds them all (no
+          // separate combine launch): each unit publishes its partial, fences,
+          // and counts itself in; the last one in reads the others from L2.
+          __syncwarp();
+          const int item = cur.seq * hkv + cur.kvh;
+          const long long first = ((cur.item_start + 1) * W - 1) / total;
+          const long long lastu = ((cur.item_start + cur.n_tiles) * W - 1) / total;
+          const int pieces = static_cast<int>(lastu - first + 1);
+          int is_last = 0;
+          if (lane == 0) {
+            __threadfence();
+            is_last = atomicAdd(&item_done[item], 1) == pieces - 1;
+            if (is_last) item_done[item] = 0;  // ready for the next launch
+          }
+          if (__shfl_sync(0xffffffffu, is_last, 0)) {
+            __threadfence();
+            const size_t base = static_cast<size_t>(item) + static_cast<size_t>(first);
+            __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + cur.kvh * g.group * kHD;
+            for (int r = 0; r < g.group; ++r) {
+              float M = -INFINITY;
+              for (int q = 0; q < pieces; ++q) M = fmaxf(M, __ldcg(part_ml + ((base + q) * g.group + r) * 2));
+              float L = 0.f;
+              float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int q = 0; q < pieces; ++q) {
+                const size_t sl = (base + q) * g.group + r;
+                const float ms = __ldcg(part_ml + sl * 2);
+                const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
+                L += __ldcg(part_ml + sl * 2 + 1) * w;
+                const float4 o4 = __ldcg(reinterpret_cast<const float4*>(part_o + sl * kHD) + lane);
+                acc.x += o4.x * w, acc.y += o4.y * w, acc.z += o4.z * w, acc.w += o4.w * w;
+              }
+              const float inv = L > 0.f ? 1.f / L : 0.f;
+              uint2 pk;
+              pk.x = pack_bf16(acc.x * inv, acc.y * inv);
+              pk.y = pack_bf16(acc.z * inv, acc.w * inv);
+              *reinterpret_cast<uint2*>(dst + r * kHD + lane * 4) = pk;
+            }
+          }
         }
       }
       pair_sync();  // staging free again (Q of the next segment lands in stage_a)
@@ -424,37 +463,6 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 // Folds the pieces of items split across warps:
 // out = sum_p 2^(m_p - M) O_p / sum_p 2^(m_p - M) l_p. CTA = (item, query
 // head), thread = head dim; items covered by a single warp are skipped.
-__global__ void decode_combine_kernel(AttnGeom g, const AttnSeq* __restrict__ seqs,
-                                      const int* __restrict__ seq_prefix, long long total, long long W,
-                                      const float* __restrict__ part_o,
-                                      const float* __restrict__ part_ml, __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const int item = blockIdx.x, r = blockIdx.y, d = threadIdx.x;
-  const int hkv = g.n_kv_heads;
-  const int seq = item / hkv, kvh = item % hkv;
-  const int n_tiles = seq_prefix[seq + 1] - seq_prefix[seq];
-  const long long s0 = static_cast<long long>(seq_prefix[seq]) * hkv + static_cast<long long>(kvh) * n_tiles;
-  const long long first = ((s0 + 1) * W - 1) / total;
-  const long long last = ((s0 + n_tiles) * W - 1) / total;
-  const int pieces = static_cast<int>(last - first + 1);
-  if (pieces <= 1) return;
-  const size_t slot0 = (static_cast<size_t>(item) + static_cast<size_t>(first)) * g.group + r;
-  float M = -INFINITY;
-  for (int q = 0; q < pieces; ++q) M = fmaxf(M, part_ml[(slot0 + static_cast<size_t>(q) * g.group) * 2]);
-  float acc = 0.f, L = 0.f;
-  for (int q = 0; q < pieces; ++q) {
-    const size_t slot = slot0 + static_cast<size_t>(q) * g.group;
-    const float ms = part_ml[slot * 2];
-    const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
-    L += part_ml[slot * 2 + 1] * w;
-    acc += part_o[slot * kHD + d] * w;
-  }
-  out[static_cast<size_t>(seqs[seq].q_start) * g.out_stride + (kvh * g.group + r) * kHD + d] =
-      __float2bfloat16(L > 0.f ? acc / L : 0.f);
-}
-
-
 }  // namespace
 
 size_t attn_smem_bytes_dec() {
@@ -467,7 +475,7 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              const AttnSeq* seqs, int n_seq, const int* seq_prefix,
                              long long total_tiles, int max_seq_tiles, const int32_t* pages,
                              __nv_bfloat16* out, float* part_o, float* part_ml, size_t part_cap,
-                             int sm_count, cudaStream_t s) {
+                             int* item_done, int sm_count, cudaStream_t s) {
   if (n_seq == 0 || total_tiles == 0) return cudaSuccess;
   if (g.group > 8) return cudaErrorInvalidValue;
   if (const cudaError_t pe = ensure_kernels_prepared(); pe != cudaSuccess) return pe;
@@ -479,20 +487,13 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if ((static_cast<size_t>(n_seq) * g.n_kv_heads + static_cast<size_t>(W)) * g.group * kHD > part_cap)
     return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  cudaError_t e = launch_pdl(decode_attn_kernel, dim3(grid), dim3(kWarpsD * 32), smem, s, g, qkv, kplane,
-                             vplane, seqs, seq_prefix, n_seq, total_tiles, W, pages, out,
-                             part_o, part_ml);
-  if (e != cudaSuccess) return e;
-  ++g_kernel_launches;
-  return launch_pdl(decode_combine_kernel, dim3(n_seq * g.n_kv_heads, g.group), dim3(kHD), 0, s, g, seqs,
-                    seq_prefix, total_tiles, W, part_o, part_ml, out);
+  return launch_pdl(decode_attn_kernel, dim3(grid), dim3(kWarpsD * 32), smem, s, g, qkv, kplane, vplane, seqs,
+                    seq_prefix, n_seq, total_tiles, W, pages, out, part_o, part_ml, item_done);
 }
 
 cudaError_t prepare_attention_kernels() {
   cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(attn_smem_bytes_dec()));
-  cudaFuncAttributes fa;
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, decode_combine_kernel);
   if (e == cudaSuccess) e = prepare_prefill_attention_kernel();
   return e;
 }

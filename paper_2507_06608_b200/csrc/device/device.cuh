@@ -214,7 +214,7 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              const AttnSeq* seqs, int n_seq, const int* seq_prefix,
                              long long total_tiles, int max_seq_tiles, const int32_t* pages,
                              __nv_bfloat16* out, float* part_o, float* part_ml, size_t part_cap,
-                             int sm_count, cudaStream_t s);
+                             int* item_done, int sm_count, cudaStream_t s);
 
 // ---- elementwise / norm / sampling (kernels.cu) ----------------------------
 cudaError_t embed(const int32_t* tokens, int n, const __nv_bfloat16* table, int hidden,

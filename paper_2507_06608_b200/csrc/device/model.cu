@@ -363,6 +363,8 @@ void LaneWs::init(Model* m, int max_tokens) {
   part_cap = static_cast<size_t>(8) << 20;  // floats
   part_o = static_cast<float*>(alloc(part_cap * 4));
   part_ml = static_cast<float*>(alloc(part_cap / a.head_dim * 2 * 4 + 1024));
+  item_done = static_cast<int*>(alloc(static_cast<size_t>(T) * m->hkv_ * 4));
+  ck(cudaMemset(item_done, 0, static_cast<size_t>(T) * m->hkv_ * 4), "item counters");
   // metadata (device + pinned mirror)
   meta_bytes = align_up(T * 12 + T * 16 + T * 8 + (static_cast<size_t>(T) + 1) * 4 * 64 +
                             static_cast<size_t>(m->cfg_.num_pages) * 4 + 4096,
@@ -629,7 +631,7 @@ void Model::forward(LaneWs& ws) {
             4.0 * ws.dec_kv_tokens * attn_cols_, [&] {
               ck(decode_attention(g, ws.qkv, kplane, vplane, ws.d_seqs, ws.dec_seq_count,
                                   ws.d_dec_prefix, ws.dec_total_tiles, ws.max_dec_tiles, ws.d_pages,
-                                  ws.attn, ws.part_o, ws.part_ml, ws.part_cap, sm, s),
+                                  ws.attn, ws.part_o, ws.part_ml, ws.part_cap, ws.item_done, sm, s),
                  "decode attention");
             });
     op = NX_OP_ATTN_PREFILL;

@@ -62,6 +62,7 @@ struct LaneWs {
   float* ws = nullptr;
   size_t ws_bytes = 0;
   float *part_o = nullptr, *part_ml = nullptr;
+  int* item_done = nullptr;  // decode attention: partials written per (sequence, kv head), zero between launches
   size_t part_cap = 0;
   CUtensorMap map_h[4], map_attn[4], map_act[4], map_hs[4];
   CUtensorMap map_q;  // q heads of the qkv buffer for prefill attention (encode_q_heads_map)
