@@ -99,6 +99,10 @@ def parse():
                         "(profiles/r01s2_gamma_*.json). Default: 5000, except 15 for the long-prompt "
                         "longbench workload where shortest-prompt-first keeps more requests under the TTFT SLO "
                         "(C3: 152 vs 117 tok/s). The reference arm runs with the same gamma")
+    p.add_argument("--decode-target-ms", type=float, default=0.0,
+                   help="nx_cost_ext.decode_target_s (x 1e-3): in prefill-priority mode a prefill share also fits "
+                        "when the decode batch's co-located step on the remaining SMs stays within this target, "
+                        "so prefill takes every SM decode does not need (0 = the reference rule alone)")
     p.add_argument("--alpha", type=float, default=1.3, help="ControllerConfig.alpha (prefill slack, paper 1.3)")
     p.add_argument("--tp", type=int, default=0,
                    help="tensor-parallel group size (C4). 0 = auto: under torchrun with --model llama3-70b the "
@@ -257,7 +261,8 @@ def load_calib(base):
 
 
 def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True, max_decode_batch=64,
-             alpha=1.3, beta=1.1, model="llama3-8b", gamma=None, static_r_p=50, tp=1, token_budget=2048):
+             alpha=1.3, beta=1.1, model="llama3-8b", gamma=None, static_r_p=50, tp=1, token_budget=2048,
+             decode_target_s=0.0):
     """tp > 1: the GpuSpec describes the TP group (peaks x tp; every GPU holds
     its kv heads of the same token pages, so the token capacity is one GPU's)."""
     m = nx.derive(*MODELS[model][0])
@@ -276,7 +281,8 @@ def make_cfg(nx, engine, num_pages, page_tokens, clock_mode, calib, bw_ext=True,
         ctrl.gamma = gamma
     return nx.sim_config(m, g, kind=kind, clock_mode=clock_mode, profile=prof, ctrl=ctrl,
                          bw_sat=bw_sat if bw_ext else None, static_r_p=static_r_p,
-                         contention=cont if bw_ext else None)
+                         contention=cont if bw_ext else None,
+                         decode_target_s=decode_target_s if bw_ext and bw_sat is not None else 0.0)
 
 
 def reference_cfg(args, num_pages, page_tokens, engine=None):
@@ -435,7 +441,7 @@ def run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_p
     def cfg_for(engine, token_budget=None):
         return make_cfg(nx, engine, num_pages, page_tokens, nx.NX_CLOCK_DEVICE, args.calib, not args.no_bw_ext,
                         args.max_decode_batch, args.alpha, args.beta, args.model, args.gamma, args.static_r_p, tp,
-                        token_budget or args.token_budget)
+                        token_budget or args.token_budget, args.decode_target_ms / 1e3)
 
     cfg = cfg_for(args.engine)
     vocab = dev.arch.vocab
@@ -625,6 +631,7 @@ def run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_p
                    "slo": {"ttft_s": args.slo_ttft, "tbt_p99_s": args.slo_tbt},
                    "max_decode_batch": args.max_decode_batch, "token_budget": args.token_budget,
                    "alpha": args.alpha, "beta": args.beta, "gamma": args.gamma,
+                   "decode_target_ms": args.decode_target_ms,
                    "kv_pool_gb": args.kv_gb,
                    "parallelism": (f"tp{tp}" + (" colocated on one GPU" if args.tp_colocated
                                                 else " (NCCL all-reduce, one process per GPU)" if tp_nccl

@@ -135,6 +135,13 @@ typedef struct nx_cost_ext {
    * (costmodel.cpp:56-64) when `contention` is set: on B200 the shared power
    * / clock budget, not HBM bandwidth, dominates the slowdown. */
   double contention_c[3];
+  /* > 0: decode-step target (seconds) of Algorithm 1's prefill-priority mode
+   * (optimizer.cpp:22-61). A prefill share also fits when the decode batch's
+   * co-located step (isolated x the contention factor above when
+   * `contention` is set) stays within this target, so prefill takes every SM
+   * the decode lane does not need to hold its step time; the reference rule
+   * (decode <= beta x T_decode(100%)) stays the floor. 0 = reference. */
+  double decode_target_s;
 } nx_cost_ext;
 
 /* SimConfig (simulator.hpp:45-51) + the cost-model extension. */

@@ -181,9 +181,12 @@ def chunked_mixed(queue, cands, budget, max_batch, chunk):  # schedulers.cpp:90-
 # ---- optimizer.cpp ---------------------------------------------------------
 
 class Controller:
-    def __init__(self, r_p, ctrl):
+    def __init__(self, r_p, ctrl, target=None):
+        """target: (decode_target_s, contention coefficients or None) of the
+        product's flagged nx_cost_ext.decode_target_s, or None = reference."""
         self.r_p, self.r_d, self.last = r_p, 100 - r_p, r_p
         self.c = ctrl
+        self.target = target
 
     def _adjust(self, target_prefill, other):  # adjust_partition, optimizer.cpp:22-61
         active, lat = other
@@ -193,17 +196,29 @@ class Controller:
         slack = self.c.beta if target_prefill else self.c.alpha
         q = 1
         bound = slack * lat(100)
+        tgt = self.target if target_prefill else None
+
+        def fits(s):
+            t = lat(100 - s)
+            if not (t > bound):
+                return True
+            if tgt is None:
+                return False
+            p = s / 100.0
+            f = 1.0 if tgt[1] is None else tgt[1][0] + tgt[1][1] * p + tgt[1][2] * p * p
+            return not (t * f > tgt[0])
+
         s = min(max(self.r_p if target_prefill else self.r_d, 1), 99)
         while True:
             q += 1
-            if not (lat(100 - s) > bound):
+            if fits(s):
                 break
             if s == 1:
                 return share_of(1), True, q
             s -= 1
         while s < 99:
             q += 1
-            if lat(100 - (s + 1)) > bound:
+            if not fits(s + 1):
                 break
             s += 1
         return share_of(s), False, q
@@ -240,7 +255,8 @@ def run_port(cfg, trace, replay=None):
     cont = list(cfg.ext.contention_c) if cfg.ext.enabled and cfg.ext.contention else None
     kind = eng.kind  # 0 nexus, 1 monolithic, 2 static
     dynamic, mono = kind == 0, kind == 1
-    ctl = Controller(eng.static_r_p if kind == 2 else 50, ctrl)
+    tgt = ((cfg.ext.decode_target_s, cont) if cfg.ext.enabled and cfg.ext.decode_target_s > 0 else None)
+    ctl = Controller(eng.static_r_p if kind == 2 else 50, ctrl, tgt)
     kvb = m.kv_bytes_per_token
     R = {r.id: dict(id=r.id, arr=r.arrival_s, P=r.prompt_len, O=r.output_len, pf=0, dc=0, adm=False, fl=False)
          for r in trace}

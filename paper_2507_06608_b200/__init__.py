@@ -90,12 +90,14 @@ def sim_config(model: ModelConfig, gpu: GpuSpec, *, kind: int = NX_ENGINE_NEXUS,
                clock_mode: int = NX_CLOCK_VIRTUAL, ctrl: ControllerConfig | None = None,
                profile: KernelProfile | None = None, timeout_sim_s: float = 3600.0,
                max_events: int = 10_000_000, bw_sat: Sequence[float] | None = None,
-               contention: Sequence[float] | None = None) -> SimConfig:
+               contention: Sequence[float] | None = None, decode_target_s: float = 0.0) -> SimConfig:
     """SimConfig; bw_sat (5 per-op shares) enables the SM-share-limited HBM
     bandwidth extension of the cost model (nx_cost_ext), None = reference;
     contention (c0, c1[, c2]) additionally replaces the contended-decode
     bandwidth split by the measured slowdown c0 + c1 p + c2 p^2 (p = the
-    prefill lane's share)."""
+    prefill lane's share); decode_target_s > 0 lets Algorithm 1's
+    prefill-priority search also accept shares whose co-located decode step
+    stays within that target (nx_cost_ext.decode_target_s)."""
     cfg = SimConfig()
     cfg.model = model
     cfg.gpu = gpu
@@ -106,13 +108,16 @@ def sim_config(model: ModelConfig, gpu: GpuSpec, *, kind: int = NX_ENGINE_NEXUS,
     e.timeout_sim_s, e.max_events = timeout_sim_s, max_events
     cfg.engine = e
     if bw_sat is not None:
-        cfg.ext = _ext(bw_sat, contention)
+        cfg.ext = _ext(bw_sat, contention, decode_target_s)
+    elif decode_target_s:
+        raise ValueError("decode_target_s needs the cost-model extension (bw_sat)")
     return cfg
 
 
-def _ext(bw_sat, contention=None) -> CostExt:
+def _ext(bw_sat, contention=None, decode_target_s=0.0) -> CostExt:
     c = (0.0, 0.0, 0.0) if contention is None else tuple(contention) + (0.0,) * (3 - len(contention))
-    return CostExt(1, 0 if contention is None else 1, (C.c_double * 5)(*bw_sat), (C.c_double * 3)(*c))
+    return CostExt(1, 0 if contention is None else 1, (C.c_double * 5)(*bw_sat), (C.c_double * 3)(*c),
+                   float(decode_target_s))
 
 
 def set_cost_ext(bw_sat: Sequence[float] | None, contention: Sequence[float] | None = None) -> None:

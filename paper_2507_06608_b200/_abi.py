@@ -63,7 +63,7 @@ class EngineConfig(C.Structure):
 
 class CostExt(C.Structure):
     _fields_ = [("enabled", C.c_int32), ("contention", C.c_int32), ("bw_sat", C.c_double * 5),
-                ("contention_c", C.c_double * 3)]
+                ("contention_c", C.c_double * 3), ("decode_target_s", C.c_double)]
 
 
 class SimConfig(C.Structure):

@@ -19,12 +19,30 @@ int select_mode(int64_t used, int64_t cap, double frac) {
                                                                      : NX_MODE_PREFILL;
 }
 
+DecodeTarget decode_target_of(const nx_cost_ext& ext) {
+  DecodeTarget dt;
+  if (ext.enabled == 0 || !(ext.decode_target_s > 0.0)) return dt;
+  dt.target_s = ext.decode_target_s;
+  dt.contention = ext.contention;
+  for (int i = 0; i < 3; ++i) dt.c[i] = ext.contention_c[i];
+  return dt;
+}
+
 // Algorithm 1 (optimizer.cpp:22-61). The target phase's share walks down
 // from its current value until the other phase fits slack * T_other(100),
 // then up while the next step still fits. Shares stay in [1, 99].
 nx_adjust_outcome adjust(int target_phase, const nx_partition_state& cur,
                          const nx_phase_model& pre, const nx_phase_model& dec,
                          const nx_controller_config& cfg) {
+  return adjust(target_phase, cur, pre, dec, cfg, DecodeTarget{});
+}
+
+// With a decode-step target (prefill-priority mode only) a prefill share
+// also fits when the decode batch's co-located step on the remaining SMs
+// stays within the target: one latency query per probe, as in the reference.
+nx_adjust_outcome adjust(int target_phase, const nx_partition_state& cur,
+                         const nx_phase_model& pre, const nx_phase_model& dec,
+                         const nx_controller_config& cfg, const DecodeTarget& dt) {
   const bool prefill_target = target_phase == NX_PHASE_PREFILL;
   const nx_phase_model& other = prefill_target ? dec : pre;
   nx_adjust_outcome out{};
@@ -39,9 +57,12 @@ nx_adjust_outcome adjust(int target_phase, const nx_partition_state& cur,
 
   int queries = 1;
   const double bound = (prefill_target ? cfg.beta : cfg.alpha) * other.latency_at(other.user, 100);
+  const bool use_target = prefill_target && dt.on();
   auto fits = [&](int target_share) {
     ++queries;
-    return !(other.latency_at(other.user, 100 - target_share) > bound);
+    const double t = other.latency_at(other.user, 100 - target_share);
+    if (!(t > bound)) return true;
+    return use_target && !(t * dt.slowdown(target_share / 100.0) > dt.target_s);
   };
   int share = std::clamp(prefill_target ? cur.r_p : cur.r_d, 1, 99);
   for (;;) {  // phase 1: shrink until the other phase meets its bound
@@ -66,7 +87,7 @@ nx_decision Controller::decide(int64_t used, int64_t cap, const nx_phase_model& 
     d.candidate_r_p = st_.r_p;
     return d;
   }
-  const nx_adjust_outcome a = adjust(target, st_, pre, dec, cfg_);
+  const nx_adjust_outcome a = adjust(target, st_, pre, dec, cfg_, dt_);
   d.candidate_r_p = a.r_p;
   d.infeasible = a.infeasible;
   d.iterations_searched = a.queries;

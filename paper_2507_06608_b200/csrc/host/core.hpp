@@ -83,9 +83,27 @@ nx_adjust_outcome adjust(int target_phase, const nx_partition_state& cur,
                          const nx_phase_model& pre, const nx_phase_model& dec,
                          const nx_controller_config& cfg);
 
+// Decode-step target of the prefill-priority search (nx_cost_ext
+// .decode_target_s; off = reference). `slowdown` maps the prefill share to
+// the co-location factor (1 without the contention term).
+struct DecodeTarget {
+  double target_s = 0.0;
+  int contention = 0;
+  double c[3] = {0.0, 0.0, 0.0};
+  bool on() const { return target_s > 0.0; }
+  double slowdown(double prefill_share) const {
+    return contention ? c[0] + c[1] * prefill_share + c[2] * prefill_share * prefill_share : 1.0;
+  }
+};
+DecodeTarget decode_target_of(const nx_cost_ext& ext);
+nx_adjust_outcome adjust(int target_phase, const nx_partition_state& cur,
+                         const nx_phase_model& pre, const nx_phase_model& dec,
+                         const nx_controller_config& cfg, const DecodeTarget& dt);
+
 class Controller {
  public:
-  Controller(nx_partition_state s, nx_controller_config c) : st_(s), cfg_(c) {}
+  Controller(nx_partition_state s, nx_controller_config c, DecodeTarget dt = {})
+      : st_(s), cfg_(c), dt_(dt) {}
   nx_decision decide(int64_t used, int64_t cap, const nx_phase_model& pre,
                      const nx_phase_model& dec);
   const nx_partition_state& state() const { return st_; }
@@ -93,6 +111,7 @@ class Controller {
  private:
   nx_partition_state st_;
   nx_controller_config cfg_;
+  DecodeTarget dt_;
 };
 
 // ---- schedulers (reference schedulers.cpp) --------------------------------

@@ -44,7 +44,7 @@ Engine::Engine(const nx_sim_config& cfg)
     : cfg_(cfg),
       dynamic_(cfg.engine.kind == NX_ENGINE_NEXUS),
       monolithic_(cfg.engine.kind == NX_ENGINE_MONOLITHIC),
-      ctl_(nx_partition_state{50, 50, 50}, cfg.ctrl) {
+      ctl_(nx_partition_state{50, 50, 50}, cfg.ctrl, decode_target_of(cfg.ext)) {
   int n_bad = 0;
   const std::string why = validate(cfg.model, cfg.gpu, cfg.ctrl, cfg.profile, &n_bad);
   if (n_bad) throw InvalidArg("invalid simulation config: " + why);

@@ -380,3 +380,32 @@ def test_contention_ext_engine_matches_port(nx):
     finally:
         nx.set_cost_ext(None)
     assert abs(co / iso - (1.05 + 0.3 * 0.75 - 0.1 * 0.75 ** 2)) < 1e-12
+
+
+def test_decode_target_ext_engine_matches_port(nx):
+    """The flagged decode-step target (nx_cost_ext.decode_target_s): in
+    prefill-priority mode a prefill share also fits when the co-located decode
+    step stays within the target. Product and port agree byte for byte, with
+    and without the contention factor; the target moves the split toward
+    prefill versus the reference rule; a zero target is the reference."""
+    from oracle.engine_port import run_port
+    m = nx.model_preset("8b")
+    g = nx.gpu_spec(148, 1.3e15, 5.5e12, 150 << 30)
+    trace = nx.workload_trace("sharegpt", 40.0, 200, 7)
+    bw = [0.45] * 5
+    plain = nx.sim_config(m, g, bw_sat=bw)
+    assert nx.run(nx.sim_config(m, g, bw_sat=bw, decode_target_s=0.0), trace).event_log == nx.run(plain, trace).event_log
+    for cont in (None, [1.05, 0.3, -0.1]):
+        cfg = nx.sim_config(m, g, bw_sat=bw, contention=cont, decode_target_s=0.03)
+        r = nx.run(cfg, trace)
+        ev, dec = run_port(cfg, trace)
+        assert r.event_log == ev and r.decision_log == dec
+
+        def mean_rp(log):
+            rows = [ln.split("\t") for ln in log.splitlines() if ln and not ln.startswith("#")]
+            return sum(int(x[4]) for x in rows) / len(rows)
+
+        base = nx.run(nx.sim_config(m, g, bw_sat=bw, contention=cont), trace)
+        assert mean_rp(r.decision_log) > mean_rp(base.decision_log)
+    with pytest.raises(ValueError):
+        nx.sim_config(m, g, decode_target_s=0.03)

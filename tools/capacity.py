@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--max-decode-batch", type=int, default=128)
     ap.add_argument("--token-budget", type=int, default=2048, help="prefill tokens per batch (both engines)")
     ap.add_argument("--kv-gb", type=float, default=80.0)
+    ap.add_argument("--decode-target-ms", type=float, default=0.0, help="nexus decode-step target (bench.py)")
     ap.add_argument("--slo-ttft", type=float, default=1.0)
     ap.add_argument("--slo-tbt", type=float, default=0.05)
     ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "capacity"))
@@ -77,7 +78,8 @@ def main():
         if name.startswith("static"):
             kind, share = "static", int(name[6:] or 50)
         return bench.make_cfg(nx, kind, num_pages, page, nx.NX_CLOCK_DEVICE, calib, True, args.max_decode_batch,
-                              1.3, args.beta, args.model, args.gamma, share, 1, args.token_budget)
+                              1.3, args.beta, args.model, args.gamma, share, 1, args.token_budget,
+                              args.decode_target_ms / 1e3 if kind == "nexus" else 0.0)
 
     def probe(name, rate):
         cfg = engine_cfg(name)
