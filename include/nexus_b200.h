@@ -39,6 +39,8 @@ extern "C" {
 const char* nx_last_error(void);
 /* Version / build identification, e.g. "nexus_b200 0.1 sm_100a". */
 const char* nx_version(void);
+/* sizeof(nx_sim_config) as compiled: FFI mirrors check their struct layout against it. */
+size_t nx_sim_config_size(void);
 
 /* ---- domain types (reference: domain.hpp:14-103) ------------------------- */
 

@@ -148,6 +148,7 @@ _PROTOS = {
     # name: (restype, argtypes)
     "nx_last_error": (C.c_char_p, []),
     "nx_version": (C.c_char_p, []),
+    "nx_sim_config_size": (C.c_size_t, []),
     "nx_model_derive": (ModelConfig, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32]),
     "nx_controller_config_default": (ControllerConfig, []),
     "nx_kernel_profile_default": (KernelProfile, []),

@@ -94,6 +94,7 @@ extern "C" {
 
 const char* nx_last_error(void) { return g_last_error.c_str(); }
 const char* nx_version(void) { return "nexus_b200 0.1 sm_100a"; }
+size_t nx_sim_config_size(void) { return sizeof(nx_sim_config); }
 
 nx_model_config nx_model_derive(int64_t d, int64_t dff, int32_t L, int32_t H, int32_t e) {
   return derive_model(d, dff, L, H, e);

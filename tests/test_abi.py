@@ -20,7 +20,8 @@ def test_struct_sizes_match_c_layout():
     assert C.sizeof(_abi.ModelConfig) == 56
     assert C.sizeof(_abi.GpuSpec) == 32
     assert C.sizeof(_abi.ControllerConfig) == 56
-    assert C.sizeof(_abi.SimConfig) == 56 + 32 + 56 + 80 + 32 + 72
+    assert C.sizeof(_abi.SimConfig) == 56 + 32 + 56 + 80 + 32 + 80
+    assert C.sizeof(_abi.SimConfig) == _abi.lib().nx_sim_config_size()
     assert C.sizeof(_abi.Breakdown) == 24 + 24 * _abi.NX_MAX_OPS
 
 
