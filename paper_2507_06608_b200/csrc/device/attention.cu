@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   const uint32_t bar_id = 1 + pair;
   auto pair_sync = [&] { named_bar_sync(bar_id, 64); };
   pdl_trigger();
-  const long long gw = static_cast<long long>(blockIdx.x) * kPairsD + pair;
+  // units are dealt to CTAs round-robin, so a short launch (W < SMs x pairs)
+  // spreads over every SM of the lane instead of filling the first CTAs
+  const long long gw = static_cast<long long>(pair) * gridDim.x + blockIdx.x;
   if (gw >= W) return;  // both warps of the pair leave together
   const long long lo = total * gw / W, hi = total * (gw + 1) / W;
   const int hkv = g.n_kv_heads;
@@ -433,16 +435,29 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
             const size_t base = static_cast<size_t>(item) + static_cast<size_t>(first);
             __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + cur.kvh * g.group * kHD;
             for (int r = 0; r < g.group; ++r) {
+              // max and denominator across the lanes (pieces strided over
+              // lanes), then every lane folds its 4 dims over all pieces with
+              // the loads of 4 pieces in flight at once (L2 latency, not
+              // bandwidth, bounds this loop)
               float M = -INFINITY;
-              for (int q = 0; q < pieces; ++q) M = fmaxf(M, __ldcg(part_ml + ((base + q) * g.group + r) * 2));
+              for (int q = lane; q < pieces; q += 32) M = fmaxf(M, __ldcg(part_ml + ((base + q) * g.group + r) * 2));
+#pragma unroll
+              for (int x = 16; x > 0; x >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, x));
               float L = 0.f;
+              for (int q = lane; q < pieces; q += 32) {
+                const size_t sl = (base + q) * g.group + r;
+                const float ms = __ldcg(part_ml + sl * 2);
+                L += ms == -INFINITY ? 0.f : __ldcg(part_ml + sl * 2 + 1) * ex2(ms - M);
+              }
+#pragma unroll
+              for (int x = 16; x > 0; x >>= 1) L += __shfl_xor_sync(0xffffffffu, L, x);
               float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
               for (int q = 0; q < pieces; ++q) {
                 const size_t sl = (base + q) * g.group + r;
                 const float ms = __ldcg(part_ml + sl * 2);
-                const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
-                L += __ldcg(part_ml + sl * 2 + 1) * w;
                 const float4 o4 = __ldcg(reinterpret_cast<const float4*>(part_o + sl * kHD) + lane);
+                const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
                 acc.x += o4.x * w, acc.y += o4.y * w, acc.z += o4.z * w, acc.w += o4.w * w;
               }
               const float inv = L > 0.f ? 1.f / L : 0.f;
@@ -480,8 +495,16 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (g.group > 8) return cudaErrorInvalidValue;
   if (const cudaError_t pe = ensure_kernels_prepared(); pe != cudaSuccess) return pe;
   const size_t smem = attn_smem_bytes_dec();
-  const long long W = std::min<long long>(static_cast<long long>(sm_count) * kPairsD, total_tiles);
-  const int grid = static_cast<int>((W + kPairsD - 1) / kPairsD);
+  // >= kMinTiles tiles per unit: a launch with fewer tiles than units would
+  // otherwise split every item into one-tile pieces whose in-kernel merge
+  // (one warp, L2 round trips per piece) costs more than the streaming
+  static const long long kMinTiles = [] {
+    const char* e = std::getenv("NX_DEC_MIN_TILES");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  const long long W = std::min<long long>(static_cast<long long>(sm_count) * kPairsD,
+                                          std::max<long long>(1, (total_tiles + kMinTiles - 1) / kMinTiles));
+  const int grid = static_cast<int>(std::min<long long>(sm_count, W));
   // compact partial slots: item + unit < n_seq * Hkv + W, independent of how
   // many pieces the longest item splits into
   if ((static_cast<size_t>(n_seq) * g.n_kv_heads + static_cast<size_t>(W)) * g.group * kHD > part_cap)
