@@ -113,7 +113,7 @@ constexpr int kTileD = kKTD * kHD;  // elements per K (or V) tile
 // the fp32 staging and the barriers must fit one SM's 227 KB opt-in
 static_assert(kPairsD >= 1 && kPairsD <= 15, "NX_DEC_PAIRS must be in [1, 15]");
 static_assert(kStD >= 1, "NX_DEC_STAGES must be >= 1");
-static_assert(static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 2 * 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
+static_assert(static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
                       kPairsD * 32 * 4 + 64 <= 227u * 1024u,
               "NX_DEC_PAIRS x NX_DEC_STAGES exceeds 227 KB of shared memory");
 
@@ -164,14 +164,16 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   extern __shared__ __align__(1024) uint8_t smem_attn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1;
-  // per pair: [kStD][K tile][V tile] + 2 x [8][128] fp32 staging (warp 0's
-  // doubles as the Q staging) + kStD barriers
-  constexpr int kPairElems = kStD * 2 * kTileD + 2 * 8 * kHD * 2;  // bf16 units
+  // per pair: [kStD][K tile][V tile] + one [8][128] fp32 staging (warp 1
+  // publishes its O there, warp 0 folds into it in place -- every element is
+  // read and rewritten by the same lane -- and it doubles as the Q staging at
+  // segment starts) + kStD barriers
+  constexpr int kPairElems = kStD * 2 * kTileD + 8 * kHD * 2;  // bf16 units
   __nv_bfloat16* pbase = reinterpret_cast<__nv_bfloat16*>(smem_attn) + pair * kPairElems;
   const uint32_t pbase_s = smem_u32(pbase);
-  __nv_bfloat16* sq = pbase + kStD * 2 * kTileD;           // Q staging [8][128] bf16 (= stage_a)
-  float* stage_a = reinterpret_cast<float*>(sq);            // [8][128] fp32, warp 0
-  float* stage_b = stage_a + 8 * kHD;                       // [8][128] fp32, warp 1
+  __nv_bfloat16* sq = pbase + kStD * 2 * kTileD;           // Q staging [8][128] bf16
+  float* stage_b = reinterpret_cast<float*>(sq);            // [8][128] fp32
+  float* stage_a = stage_b;                                 // merged (m, l, O), in place
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(smem_attn) +
                                                kPairsD * kPairElems) + pair * kStD;
   // empty[s]: both warps of the pair are done reading stage s (2 arrivals); only
@@ -205,13 +207,23 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   DecPos prod = dec_locate(seq_prefix, n_seq, hkv, lo);
   long long issued = lo;
   int nxt_pg0 = 0, nxt_pg1 = 0, nxt_kvh = 0;
+  // the producer's sequence record is re-read only when its cursor enters a
+  // new sequence, so a refill's lookup is one dependent load (the page ids),
+  // not a chain (record -> page ids)
+  int pm_seq = -1, pm_kv_len = 0;
+  const int32_t* pm_pt = pages;
   auto lookup = [&]() {
-    const AttnSeq ms = seqs[prod.seq];
-    const int32_t* pt = pages + ms.page_off;
-    const int last = pt[(ms.kv_len - 1) >> 4];  // keys past kv_len re-load it (masked, finite)
+    if (prod.seq != pm_seq) {
+      const AttnSeq ms = seqs[prod.seq];
+      pm_seq = prod.seq;
+      pm_kv_len = ms.kv_len;
+      pm_pt = pages + ms.page_off;
+    }
+    // a tile starts below kv_len; a second half past it re-loads the first
+    // half's page (masked, finite)
     const int key = prod.tile * kKTD;
-    nxt_pg0 = key < ms.kv_len ? pt[key >> 4] : last;
-    nxt_pg1 = key + 16 < ms.kv_len ? pt[(key + 16) >> 4] : last;
+    nxt_pg0 = pm_pt[key >> 4];
+    nxt_pg1 = key + 16 < pm_kv_len ? pm_pt[(key + 16) >> 4] : nxt_pg0;
     nxt_kvh = prod.kvh;
   };
   auto issue = [&](int st) {
@@ -469,7 +481,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
           }
         }
       }
-      pair_sync();  // staging free again (Q of the next segment lands in stage_a)
+      pair_sync();  // staging free again (Q of the next segment lands there)
     }
     dec_advance(cur, seq_prefix, n_seq, hkv);
   }
@@ -481,7 +493,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 }  // namespace
 
 size_t attn_smem_bytes_dec() {
-  return static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 2 * 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
+  return static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
          kPairsD * 32 * 4 + 64;
 }
 
