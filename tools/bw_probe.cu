@@ -81,9 +81,32 @@ int main() {
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   struct Cfg { int mode, chunk, stages; };
   std::vector<Cfg> cfgs = {{1, 16384, 12}, {1, 4096, 48}, {1, 4096, 12}, {2, 16384, 12}, {2, 16384, 6}, {1, 32768, 6}};
+  std::vector<int> sm_list = {16, 48, 148};
+  // BW_CFGS="mode:chunk:stages,..." and BW_SMS="32,148" override the sweep
+  if (const char* e = getenv("BW_CFGS")) {
+    cfgs.clear();
+    for (const char* q = e; *q;) {
+      Cfg c;
+      int n = 0;
+      if (sscanf(q, "%d:%d:%d%n", &c.mode, &c.chunk, &c.stages, &n) != 3) break;
+      cfgs.push_back(c);
+      q += n;
+      if (*q == ',') ++q;
+    }
+  }
+  if (const char* e = getenv("BW_SMS")) {
+    sm_list.clear();
+    for (const char* q = e; *q;) {
+      int v = 0, n = 0;
+      if (sscanf(q, "%d%n", &v, &n) != 1) break;
+      sm_list.push_back(v);
+      q += n;
+      if (*q == ',') ++q;
+    }
+  }
   const long long total_bytes = 2ll << 30;
   for (auto c : cfgs) {
-    for (int sms : {16, 48, 148}) {
+    for (int sms : sm_list) {
       long long chunks = total_bytes / c.chunk;
       if (sms <= 16) chunks /= 8;
       int smem = c.stages * c.chunk + 1024;
