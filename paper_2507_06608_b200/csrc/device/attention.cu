@@ -107,7 +107,6 @@ constexpr int kKTD = 32;      // keys per decode tile (two 16-token pages)
 #endif
 constexpr int kStD = NX_DEC_STAGES;   // ring stages per pair
 constexpr int kPairsD = NX_DEC_PAIRS; // warp pairs per CTA (one CTA per SM)
-constexpr int kWarpsD = 2 * kPairsD;
 constexpr int kTileD = kKTD * kHD;  // elements per K (or V) tile
 // named barrier 1 + pair must stay below the 16 hardware barriers; the ring,
 // the fp32 staging and the barriers must fit one SM's 227 KB opt-in
@@ -116,6 +115,31 @@ static_assert(kStD >= 1, "NX_DEC_STAGES must be >= 1");
 static_assert(static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
                       kPairsD * 32 * 4 + 64 <= 227u * 1024u,
               "NX_DEC_PAIRS x NX_DEC_STAGES exceeds 227 KB of shared memory");
+
+// Head-pair items (HP = 2, even kv-head counts): one unit streams two kv heads
+// of a sequence together, so every page refill is one 16 KB copy of two
+// adjacent (page, kv head) blocks instead of two 8 KB copies; warp h of the
+// pair owns kv head 2 hg + h over all 32 keys of a tile, so no pair merge.
+// Bulk copies pay a per-copy cost: one issuing thread moves 55 / 109 / 182
+// GB/s per SM with 8 / 16 / 32 KB copies on a 32-SM lane
+// (profiles/r02_bw_probe_copy_size.jsonl).
+#ifndef NX_DEC_PAIRS_HP2
+#define NX_DEC_PAIRS_HP2 5
+#endif
+template <int HP>
+struct DecCfg {
+  static constexpr int kPairs = HP == 1 ? kPairsD : NX_DEC_PAIRS_HP2;
+  static constexpr int kSt = HP == 1 ? kStD : 1;
+  // ring stage (2 pages x HP blocks) and staging (HP = 1: Q / fp32 shared;
+  // HP = 2: Q [16][128] bf16, then one [8][128] fp32 per warp), bf16 units
+  static constexpr int kStageElems = 2 * HP * kKVBlock;
+  static constexpr int kStagingElems = HP == 1 ? 8 * kHD * 2 : 3 * 8 * kHD * 2;
+  static constexpr int kPairElems = kSt * kStageElems + kStagingElems;
+  static constexpr size_t kSmem = static_cast<size_t>(kPairs) * kPairElems * 2 + 2 * kPairs * kSt * 8 +
+                                  kPairs * 32 * 4 + 64;
+};
+static_assert(DecCfg<2>::kPairs >= 1 && DecCfg<2>::kPairs <= 15, "NX_DEC_PAIRS_HP2 must be in [1, 15]");
+static_assert(DecCfg<2>::kSmem <= 227u * 1024u, "NX_DEC_PAIRS_HP2 exceeds 227 KB of shared memory");
 
 
 // Item (sequence, kv head) holding flattened tile index gt: seq_prefix[s] is
@@ -153,7 +177,8 @@ __device__ __forceinline__ void dec_advance(DecPos& d, const int* __restrict__ s
   }
 }
 
-__global__ void __launch_bounds__(kWarpsD * 32, 1)
+template <int HP>
+__global__ void __launch_bounds__(2 * DecCfg<HP>::kPairs * 32, 1)
     decode_attn_kernel(AttnGeom g, const __nv_bfloat16* __restrict__ qkv,
                        const __nv_bfloat16* __restrict__ kplane,
                        const __nv_bfloat16* __restrict__ vplane, const AttnSeq* __restrict__ seqs,
@@ -168,18 +193,21 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   // publishes its O there, warp 0 folds into it in place -- every element is
   // read and rewritten by the same lane -- and it doubles as the Q staging at
   // segment starts) + kStD barriers
-  constexpr int kPairElems = kStD * 2 * kTileD + 8 * kHD * 2;  // bf16 units
+  // (HP = 2: separate Q and per-warp output staging, see DecCfg)
+  constexpr int kPairs = DecCfg<HP>::kPairs, kSt = DecCfg<HP>::kSt;
+  constexpr int kPairElems = DecCfg<HP>::kPairElems;  // bf16 units
   __nv_bfloat16* pbase = reinterpret_cast<__nv_bfloat16*>(smem_attn) + pair * kPairElems;
   const uint32_t pbase_s = smem_u32(pbase);
-  __nv_bfloat16* sq = pbase + kStD * 2 * kTileD;           // Q staging [8][128] bf16
-  float* stage_b = reinterpret_cast<float*>(sq);            // [8][128] fp32
+  __nv_bfloat16* sq = pbase + kSt * DecCfg<HP>::kStageElems;  // Q staging [HP x 8][128] bf16
+  float* stage_b = HP == 1 ? reinterpret_cast<float*>(sq)     // [8][128] fp32
+                           : reinterpret_cast<float*>(sq + 8 * kHD * 2) + half * 8 * kHD;
   float* stage_a = stage_b;                                 // merged (m, l, O), in place
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(smem_attn) +
-                                               kPairsD * kPairElems) + pair * kStD;
+                                               kPairs * kPairElems) + pair * kSt;
   // empty[s]: both warps of the pair are done reading stage s (2 arrivals); only
   // the producer waits on it, so neither warp stalls on the other per tile
-  uint64_t* empty = full + kPairsD * kStD;
-  float* ml_b = reinterpret_cast<float*>(full + 2 * kPairsD * kStD - pair * kStD) + pair * 32;  // [8 heads][m, l]
+  uint64_t* empty = full + kPairs * kSt;
+  float* ml_b = reinterpret_cast<float*>(full + 2 * kPairs * kSt - pair * kSt) + pair * 32;  // [8 heads][m, l]
   const uint32_t bar_id = 1 + pair;
   auto pair_sync = [&] { named_bar_sync(bar_id, 64); };
   pdl_trigger();
@@ -189,9 +217,10 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   if (gw >= W) return;  // both warps of the pair leave together
   const long long lo = total * gw / W, hi = total * (gw + 1) / W;
   const int hkv = g.n_kv_heads;
+  const int hkv_g = hkv / HP;  // items per sequence (kv heads or head pairs)
   const bool producer = half == 0 && lane == 0;
   if (producer) {
-    for (int i = 0; i < kStD; ++i) {
+    for (int i = 0; i < kSt; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 2);
     }
@@ -204,7 +233,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   // the page ids of the next tile to issue are looked up one refill ahead, so
   // the dependent global loads (sequence -> page table -> page) overlap a tile
   // of compute instead of stalling the producer's warp at every refill
-  DecPos prod = dec_locate(seq_prefix, n_seq, hkv, lo);
+  DecPos prod = dec_locate(seq_prefix, n_seq, hkv_g, lo);
   long long issued = lo;
   int nxt_pg0 = 0, nxt_pg1 = 0, nxt_kvh = 0;
   // the producer's sequence record is re-read only when its cursor enters a
@@ -227,21 +256,22 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
     nxt_kvh = prod.kvh;
   };
   auto issue = [&](int st) {
-    __nv_bfloat16* dst = pbase + st * 2 * kTileD;
-    mbar_expect_tx(&full[st], 2 * 2 * 4096);
-    bulk_load(dst, kplane + (static_cast<size_t>(nxt_pg0) * hkv + nxt_kvh) * kKVBlock, 8192, &full[st], pol);
-    bulk_load(dst + kKVBlock, kplane + (static_cast<size_t>(nxt_pg1) * hkv + nxt_kvh) * kKVBlock, 8192, &full[st],
+    __nv_bfloat16* dst = pbase + st * DecCfg<HP>::kStageElems;
+    mbar_expect_tx(&full[st], 2 * HP * 8192);
+    bulk_load(dst, kplane + (static_cast<size_t>(nxt_pg0) * hkv + nxt_kvh * HP) * kKVBlock, HP * 8192, &full[st],
               pol);
+    bulk_load(dst + HP * kKVBlock, kplane + (static_cast<size_t>(nxt_pg1) * hkv + nxt_kvh * HP) * kKVBlock,
+              HP * 8192, &full[st], pol);
   };
   if (producer) {
-    for (; issued < hi && issued < lo + kStD; ++issued) {
+    for (; issued < hi && issued < lo + kSt; ++issued) {
       lookup();
       issue(static_cast<int>(issued - lo));
-      dec_advance(prod, seq_prefix, n_seq, hkv);
+      dec_advance(prod, seq_prefix, n_seq, hkv_g);
     }
     if (issued < hi) lookup();
   }
-  DecPos cur = dec_locate(seq_prefix, n_seq, hkv, lo);
+  DecPos cur = dec_locate(seq_prefix, n_seq, hkv_g, lo);
   // Transposed tile math: S^T = K Q^T and O^T += V^T P^T, so keys / head
   // dims are the MMA's 16-row M side and the <= 8 query heads of the GQA
   // group its N = 8 side (half the m16n8k16 count of Q-as-rows, where 16 MMA
@@ -252,39 +282,42 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
   AttnSeq meta = seqs[cur.seq];
   int seg_tile0 = cur.tile;
   const int h0 = 2 * (lane & 3);
-  const int krow = half * 16;  // this warp's 16 keys of every tile
   // ldmatrix lane addresses, hoisted: in a 1 KB atom (8 rows x 128 B), chunk
   // (2 k + b) & 7 of row r sits at r * 128 + ((2 k + b) ^ r) << 4 =
   // (b ^ (r & 1)) << 4 | ((k ^ g) << 5) with g = (r & 6) >> 1, so 4 per-lane
   // bases cover k = 0..3; dims 64..127 (k & 4) are the next atom, +1 KB, and
-  // token rows 8..15 the atom pair 2 KB on (kv_chunk_elem). K: row 2 krow + (lane & 7) + 8 b3, chunk b = lane >> 4;
-  // V (trans): row 2 krow + (lane & 7) + 8 (lane >> 4), chunk b = b3.
+  // token rows 8..15 the atom pair 2 KB on (kv_chunk_elem). K: row (lane & 7) + 8 b3, chunk b = lane >> 4;
+  // V (trans): row (lane & 7) + 8 (lane >> 4), chunk b = b3; relative to the
+  // page block of the sub-tile (added at use).
   const int l7 = lane & 7, b3 = (lane >> 3) & 1, b4 = lane >> 4, gx = (l7 & 6) >> 1;
   uint32_t koff[4], voff[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    koff[j] = static_cast<uint32_t>(krow * 512 + b3 * 2048 + l7 * 128 + (((b4 ^ l7) & 1) << 4) + ((j ^ gx) << 5));
-    voff[j] = static_cast<uint32_t>(krow * 512 + 4096 + b4 * 2048 + l7 * 128 + (((b3 ^ l7) & 1) << 4) +
+    koff[j] = static_cast<uint32_t>(b3 * 2048 + l7 * 128 + (((b4 ^ l7) & 1) << 4) + ((j ^ gx) << 5));
+    voff[j] = static_cast<uint32_t>(4096 + b4 * 2048 + l7 * 128 + (((b3 ^ l7) & 1) << 4) +
                                     ((j ^ gx) << 5));
   }
   for (long long gt = lo; gt < hi; ++gt) {
-    const int i = static_cast<int>(gt - lo), buf = i % kStD;
+    const int i = static_cast<int>(gt - lo), buf = i % kSt;
     if (gt == lo || cur.tile == 0) {  // new segment: this item's queries
       meta = seqs[cur.seq];
       seg_tile0 = cur.tile;
-      for (int c = half * 32 + lane; c < 8 * 16; c += 64) {
-        const int r = c >> 4, chunk = c & 15;
+      // rows 8 hh + q: query head q of the item's kv head hh (HP = 2: warp h
+      // takes rows 8 h ..)
+      for (int c = half * 32 + lane; c < HP * 8 * 16; c += 64) {
+        const int r = c >> 4, chunk = c & 15, hh = r >> 3, qr = r & 7;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (r < g.group)
+        if (qr < g.group)
           v = *reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(meta.q_start) * g.qkv_stride +
-                                              (cur.kvh * g.group + r) * kHD + chunk * 8);
+                                              ((cur.kvh * HP + hh) * g.group + qr) * kHD + chunk * 8);
         *reinterpret_cast<uint4*>(sq + r * kHD + ((chunk ^ (r & 7)) << 3)) = v;
       }
       pair_sync();
+      const __nv_bfloat16* sqw = sq + (HP == 2 ? half * 8 * kHD : 0);
 #pragma unroll
       for (int k = 0; k < 8; k += 2) {
         uint32_t r[4];
-        ldsm_x4(r, sq + swz(lane & 7, k * 16 + ((lane >> 3) << 3)));
+        ldsm_x4(r, sqw + swz(lane & 7, k * 16 + ((lane >> 3) << 3)));
         qb[k][0] = r[0], qb[k][1] = r[1], qb[k + 1][0] = r[2], qb[k + 1][1] = r[3];
       }
       m0 = m1 = -INFINITY;
@@ -292,10 +325,16 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 #pragma unroll
       for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     }
-    mbar_wait(&full[buf], (i / kStD) & 1);
-    // [2 blocks][K 16 | V 16][128]; shared-window byte address of the stage
-    const uint32_t sbase = pbase_s + static_cast<uint32_t>(buf * 2 * kTileD * 2);
-    // S^T = K Q^T over this warp's 16 keys: 8 k-steps in two chains
+    mbar_wait(&full[buf], (i / kSt) & 1);
+    // [2 pages][HP kv heads][K 16 | V 16][128]; shared-window byte address of the stage
+    const uint32_t sbase0 = pbase_s + static_cast<uint32_t>(buf * DecCfg<HP>::kStageElems * 2);
+    // HP = 1: warp h takes page h of the tile (keys 16 h ..); HP = 2: warp h
+    // takes its kv head's block of both pages, one 16-key sub-tile after the other
+#pragma unroll
+    for (int j = 0; j < HP; ++j) {
+    const int sub = HP == 1 ? half : j;
+    const uint32_t sbase = sbase0 + static_cast<uint32_t>(sub * HP * 8192 + (HP == 2 ? half * 8192 : 0));
+    // S^T = K Q^T over 16 keys: 8 k-steps
     // four independent accumulation chains of two MMAs (HMMA latency, not issue, bounds a chain)
     float sc[4][4];
 #pragma unroll
@@ -310,7 +349,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 #pragma unroll
     for (int j = 0; j < 4; ++j) s[j] = (sc[0][j] + sc[1][j]) + (sc[2][j] + sc[3][j]);
     // mask keys past kv_len; online softmax down each head column
-    const int key0 = cur.tile * kKTD + krow + (lane >> 2);
+    const int key0 = cur.tile * kKTD + sub * 16 + (lane >> 2);
     float mx0 = m0, mx1 = m1;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -347,13 +386,14 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
       ldsm_x4_t_s(a, sbase + voff[db & 3] + ((db & 4) << 8));
       mma16816(o[db], a, pb0, pb1);
     }
+    }  // sub-tiles
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with stage buf
-    // refill this stage kStD tiles ahead, once both warps released it
+    // refill this stage kSt tiles ahead, once both warps released it
     if (producer && issued < hi) {
-      mbar_wait(&empty[buf], static_cast<uint32_t>((i / kStD) & 1));
+      mbar_wait(&empty[buf], static_cast<uint32_t>((i / kSt) & 1));
       issue(buf);
-      dec_advance(prod, seq_prefix, n_seq, hkv);
+      dec_advance(prod, seq_prefix, n_seq, hkv_g);
       if (++issued < hi) lookup();
     }
     // segment end: last tile of the item or of this unit's range
@@ -365,8 +405,9 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
         lt0 += __shfl_xor_sync(0xffffffff, lt0, x);
         lt1 += __shfl_xor_sync(0xffffffff, lt1, x);
       }
-      // merge the pair: warp 1 publishes (m, l, O), warp 0 folds
-      if (half == 1) {
+      // HP = 1: merge the pair (warp 1 publishes (m, l, O), warp 0 folds);
+      // HP = 2: each warp finalizes its own kv head
+      if (HP == 1 && half == 1) {
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
           const int dim = d * 16 + (lane >> 2);
@@ -380,10 +421,11 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
           ml_b[(h0 + 1) * 2] = m1, ml_b[(h0 + 1) * 2 + 1] = lt1;
         }
       }
-      pair_sync();
-      if (half == 0) {
-        const float mb0 = ml_b[h0 * 2], lb0 = ml_b[h0 * 2 + 1];
-        const float mb1 = ml_b[(h0 + 1) * 2], lb1 = ml_b[(h0 + 1) * 2 + 1];
+      if (HP == 1) pair_sync();
+      if (HP == 2 || half == 0) {
+        const int kvh_w = cur.kvh * HP + (HP == 2 ? half : 0);  // this warp's kv head
+        const float mb0 = HP == 1 ? ml_b[h0 * 2] : -INFINITY, lb0 = HP == 1 ? ml_b[h0 * 2 + 1] : 0.f;
+        const float mb1 = HP == 1 ? ml_b[(h0 + 1) * 2] : -INFINITY, lb1 = HP == 1 ? ml_b[(h0 + 1) * 2 + 1] : 0.f;
         const float M0 = fmaxf(m0, mb0), M1 = fmaxf(m1, mb1);
         const float fa0 = m0 == -INFINITY ? 0.f : ex2(m0 - M0), fb0 = mb0 == -INFINITY ? 0.f : ex2(mb0 - M0);
         const float fa1 = m1 == -INFINITY ? 0.f : ex2(m1 - M1), fb1 = mb1 == -INFINITY ? 0.f : ex2(mb1 - M1);
@@ -396,14 +438,21 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
           const int dim = d * 16 + (lane >> 2);
-          stage_a[h0 * kHD + dim] = o[d][0] * sa0 + stage_b[h0 * kHD + dim] * sb0;
-          stage_a[(h0 + 1) * kHD + dim] = o[d][1] * sa1 + stage_b[(h0 + 1) * kHD + dim] * sb1;
-          stage_a[h0 * kHD + dim + 8] = o[d][2] * sa0 + stage_b[h0 * kHD + dim + 8] * sb0;
-          stage_a[(h0 + 1) * kHD + dim + 8] = o[d][3] * sa1 + stage_b[(h0 + 1) * kHD + dim + 8] * sb1;
+          if (HP == 1) {
+            stage_a[h0 * kHD + dim] = o[d][0] * sa0 + stage_b[h0 * kHD + dim] * sb0;
+            stage_a[(h0 + 1) * kHD + dim] = o[d][1] * sa1 + stage_b[(h0 + 1) * kHD + dim] * sb1;
+            stage_a[h0 * kHD + dim + 8] = o[d][2] * sa0 + stage_b[h0 * kHD + dim + 8] * sb0;
+            stage_a[(h0 + 1) * kHD + dim + 8] = o[d][3] * sa1 + stage_b[(h0 + 1) * kHD + dim + 8] * sb1;
+          } else {
+            stage_a[h0 * kHD + dim] = o[d][0] * sa0;
+            stage_a[(h0 + 1) * kHD + dim] = o[d][1] * sa1;
+            stage_a[h0 * kHD + dim + 8] = o[d][2] * sa0;
+            stage_a[(h0 + 1) * kHD + dim + 8] = o[d][3] * sa1;
+          }
         }
         __syncwarp();
         if (whole) {
-          __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + cur.kvh * g.group * kHD;
+          __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + kvh_w * g.group * kHD;
           for (int c = lane; c < g.group * 16; c += 32) {
             const float4 u = *reinterpret_cast<const float4*>(stage_a + c * 8);
             const float4 v = *reinterpret_cast<const float4*>(stage_a + c * 8 + 4);
@@ -414,8 +463,10 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
         } else {
           // compact partial slot: item + unit. The units of item k are
           // [first_k, last_k] with first_{k+1} >= last_k, so item + unit is unique
-          // per (item, unit) and below n_items + W (the combine reads item + first + q)
-          const size_t slot = static_cast<size_t>(cur.seq) * hkv + cur.kvh + static_cast<size_t>(gw);
+          // per (item, unit) and below n_items + W (the combine reads item + first + q);
+          // HP heads per item slot
+          const size_t slot =
+              (static_cast<size_t>(cur.seq) * hkv_g + cur.kvh + static_cast<size_t>(gw)) * HP + (HP == 2 ? half : 0);
           float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
           for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(stage_a + c * 4);
           if (lane < 4) {
@@ -432,7 +483,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
           // separate combine launch): each unit publishes its partial, fences,
           // and counts itself in; the last one in reads the others from L2.
           __syncwarp();
-          const int item = cur.seq * hkv + cur.kvh;
+          const int item = cur.seq * hkv + kvh_w;  // completion count per kv head
           const long long first = ((cur.item_start + 1) * W - 1) / total;
           const long long lastu = ((cur.item_start + cur.n_tiles) * W - 1) / total;
           const int pieces = static_cast<int>(lastu - first + 1);
@@ -444,20 +495,22 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
           }
           if (__shfl_sync(0xffffffffu, is_last, 0)) {
             __threadfence();
-            const size_t base = static_cast<size_t>(item) + static_cast<size_t>(first);
-            __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + cur.kvh * g.group * kHD;
+            const size_t base = static_cast<size_t>(cur.seq) * hkv_g + cur.kvh + static_cast<size_t>(first);
+            const size_t hw = HP == 2 ? half : 0;
+            __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + kvh_w * g.group * kHD;
             for (int r = 0; r < g.group; ++r) {
               // max and denominator across the lanes (pieces strided over
               // lanes), then every lane folds its 4 dims over all pieces with
               // the loads of 4 pieces in flight at once (L2 latency, not
               // bandwidth, bounds this loop)
               float M = -INFINITY;
-              for (int q = lane; q < pieces; q += 32) M = fmaxf(M, __ldcg(part_ml + ((base + q) * g.group + r) * 2));
+              for (int q = lane; q < pieces; q += 32)
+                M = fmaxf(M, __ldcg(part_ml + (((base + q) * HP + hw) * g.group + r) * 2));
 #pragma unroll
               for (int x = 16; x > 0; x >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, x));
               float L = 0.f;
               for (int q = lane; q < pieces; q += 32) {
-                const size_t sl = (base + q) * g.group + r;
+                const size_t sl = ((base + q) * HP + hw) * g.group + r;
                 const float ms = __ldcg(part_ml + sl * 2);
                 L += ms == -INFINITY ? 0.f : __ldcg(part_ml + sl * 2 + 1) * ex2(ms - M);
               }
@@ -466,7 +519,7 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
               float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
               for (int q = 0; q < pieces; ++q) {
-                const size_t sl = (base + q) * g.group + r;
+                const size_t sl = ((base + q) * HP + hw) * g.group + r;
                 const float ms = __ldcg(part_ml + sl * 2);
                 const float4 o4 = __ldcg(reinterpret_cast<const float4*>(part_o + sl * kHD) + lane);
                 const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
@@ -483,19 +536,27 @@ __global__ void __launch_bounds__(kWarpsD * 32, 1)
       }
       pair_sync();  // staging free again (Q of the next segment lands there)
     }
-    dec_advance(cur, seq_prefix, n_seq, hkv);
+    dec_advance(cur, seq_prefix, n_seq, hkv_g);
   }
 }
 
-// Folds the pieces of items split across warps:
-// out = sum_p 2^(m_p - M) O_p / sum_p 2^(m_p - M) l_p. CTA = (item, query
-// head), thread = head dim; items covered by a single warp are skipped.
+// Items of HP kv heads: head pairs on lanes of >= 96 SMs when the kv-head
+// count is even (NX_DEC_HP=1 / 2 forces one form where it applies). Measured
+// (profiles/r02_attn_decode_variants_ab.jsonl, 8B): on the whole GPU head
+// pairs stream short launches 15% and B = 128 x ctx 600 4% faster; on a
+// 32-SM lane both forms run at ~90 GB/s per SM (every unit waits on its
+// one-stage refill) and single heads are up to 5% ahead.
+int decode_heads_per_item(int n_kv_heads, int sm_count) {
+  static const int force = [] {
+    const char* e = std::getenv("NX_DEC_HP");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (n_kv_heads % 2 != 0 || force == 1) return 1;
+  return force == 2 || sm_count >= 96 ? 2 : 1;
+}
 }  // namespace
 
-size_t attn_smem_bytes_dec() {
-  return static_cast<size_t>(kPairsD) * (kStD * 2 * kTileD + 8 * kHD * 2) * 2 + 2 * kPairsD * kStD * 8 +
-         kPairsD * 32 * 4 + 64;
-}
+size_t attn_smem_bytes_dec() { return DecCfg<1>::kSmem; }
 
 cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
                              const __nv_bfloat16* kplane, const __nv_bfloat16* vplane,
@@ -506,7 +567,10 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (n_seq == 0 || total_tiles == 0) return cudaSuccess;
   if (g.group > 8) return cudaErrorInvalidValue;
   if (const cudaError_t pe = ensure_kernels_prepared(); pe != cudaSuccess) return pe;
-  const size_t smem = attn_smem_bytes_dec();
+  const int HP = decode_heads_per_item(g.n_kv_heads, sm_count);
+  const int pairs = HP == 2 ? DecCfg<2>::kPairs : DecCfg<1>::kPairs;
+  const size_t smem = HP == 2 ? DecCfg<2>::kSmem : DecCfg<1>::kSmem;
+  total_tiles /= HP;  // the caller counts tiles per kv head; items hold HP heads
   // >= kMinTiles tiles per unit: a launch with fewer tiles than units would
   // otherwise split every item into one-tile pieces whose in-kernel merge
   // (one warp, L2 round trips per piece) costs more than the streaming
@@ -514,21 +578,27 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
     const char* e = std::getenv("NX_DEC_MIN_TILES");
     return e ? std::max(1, std::atoi(e)) : 4;
   }();
-  const long long W = std::min<long long>(static_cast<long long>(sm_count) * kPairsD,
+  const long long W = std::min<long long>(static_cast<long long>(sm_count) * pairs,
                                           std::max<long long>(1, (total_tiles + kMinTiles - 1) / kMinTiles));
   const int grid = static_cast<int>(std::min<long long>(sm_count, W));
-  // compact partial slots: item + unit < n_seq * Hkv + W, independent of how
-  // many pieces the longest item splits into
-  if ((static_cast<size_t>(n_seq) * g.n_kv_heads + static_cast<size_t>(W)) * g.group * kHD > part_cap)
+  // compact partial slots: (item + unit) x HP heads < (n_seq * Hkv / HP + W) x
+  // HP, independent of how many pieces the longest item splits into
+  if ((static_cast<size_t>(n_seq) * (g.n_kv_heads / HP) + static_cast<size_t>(W)) * HP * g.group * kHD > part_cap)
     return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  return launch_pdl(decode_attn_kernel, dim3(grid), dim3(kWarpsD * 32), smem, s, g, qkv, kplane, vplane, seqs,
-                    seq_prefix, n_seq, total_tiles, W, pages, out, part_o, part_ml, item_done);
+  const dim3 block(2 * pairs * 32);
+  return HP == 2 ? launch_pdl(decode_attn_kernel<2>, dim3(grid), block, smem, s, g, qkv, kplane, vplane, seqs,
+                              seq_prefix, n_seq, total_tiles, W, pages, out, part_o, part_ml, item_done)
+                 : launch_pdl(decode_attn_kernel<1>, dim3(grid), block, smem, s, g, qkv, kplane, vplane, seqs,
+                              seq_prefix, n_seq, total_tiles, W, pages, out, part_o, part_ml, item_done);
 }
 
 cudaError_t prepare_attention_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(attn_smem_bytes_dec()));
+  cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(DecCfg<1>::kSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(decode_attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(DecCfg<2>::kSmem));
   if (e == cudaSuccess) e = prepare_prefill_attention_kernel();
   return e;
 }

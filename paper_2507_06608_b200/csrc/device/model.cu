@@ -73,27 +73,31 @@ void Partitions::init(int device, bool enable) {
   CUdevResource all;
   if (get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
     throw std::runtime_error("cuDeviceGetDevResource");
-  // Decode lane takes a group of 8k SMs (the green-context granularity on
-  // sm_90+), the prefill lane the remaining SMs of the same split.
-  for (int k = 1; 8 * k + 8 <= static_cast<int>(all.sm.smCount) && k <= 31; ++k) {
-    CUdevResource grp, rest;
-    unsigned n = 1;
-    if (split(&grp, &n, &all, &rest, 0, 8 * k) != CUDA_SUCCESS || n != 1) break;
+  auto add_layout = [&](const CUdevResource* dec, unsigned n_dec, const CUdevResource* pre, unsigned n_pre) {
     CUdevResourceDesc dg, dr;
     CUgreenCtx gg, gr;
     CUstream sg, sr;
-    if (gen(&dg, &grp, 1) != CUDA_SUCCESS || gen(&dr, &rest, 1) != CUDA_SUCCESS ||
+    if (gen(&dg, const_cast<CUdevResource*>(dec), n_dec) != CUDA_SUCCESS ||
+        gen(&dr, const_cast<CUdevResource*>(pre), n_pre) != CUDA_SUCCESS ||
         create(&gg, dg, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
         create(&gr, dr, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
         mkstream(&sg, gg, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
         mkstream(&sr, gr, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
       throw std::runtime_error("green context creation failed");
     Layout l;
-    l.decode_sms = static_cast<int>(grp.sm.smCount);
-    l.prefill_sms = static_cast<int>(rest.sm.smCount);
+    for (unsigned i = 0; i < n_dec; ++i) l.decode_sms += static_cast<int>(dec[i].sm.smCount);
+    for (unsigned i = 0; i < n_pre; ++i) l.prefill_sms += static_cast<int>(pre[i].sm.smCount);
     l.decode_stream = reinterpret_cast<cudaStream_t>(sg);
     l.prefill_stream = reinterpret_cast<cudaStream_t>(sr);
     layouts.push_back(l);
+  };
+  // Decode lane takes a group of 8k SMs (the green-context granularity on
+  // sm_90+), the prefill lane the remaining SMs of the same split.
+  for (int k = 1; 8 * k + 8 <= static_cast<int>(all.sm.smCount) && k <= 31; ++k) {
+    CUdevResource grp, rest;
+    unsigned n = 1;
+    if (split(&grp, &n, &all, &rest, 0, 8 * k) != CUDA_SUCCESS || n != 1) break;
+    add_layout(&grp, 1, &rest, 1);
   }
   enabled = !layouts.empty();
 }
