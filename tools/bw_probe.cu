@@ -79,6 +79,41 @@ int main() {
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encode fail\n"); return 1; }
   CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  // BW_GREEN=contig|spread: launch into a green-context partition of
+  // BW_GREEN_SMS SMs (the first 8k SMs of a split, or k of the 8-SM groups
+  // spaced evenly over the split) instead of a plain stream
+  cudaStream_t gstream = 0;
+  const char* gmode = getenv("BW_GREEN");
+  if (gmode) {
+    auto sym = [](const char* name) {
+      void* p = nullptr; cudaDriverEntryPointQueryResult qq;
+      CK(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &qq));
+      return p;
+    };
+    auto get_res = (PFN_cuDeviceGetDevResource)sym("cuDeviceGetDevResource");
+    auto split = (PFN_cuDevSmResourceSplitByCount)sym("cuDevSmResourceSplitByCount");
+    auto gen = (PFN_cuDevResourceGenerateDesc)sym("cuDevResourceGenerateDesc");
+    auto create = (PFN_cuGreenCtxCreate)sym("cuGreenCtxCreate");
+    auto mkstream = (PFN_cuGreenCtxStreamCreate)sym("cuGreenCtxStreamCreate");
+    CUdevice dev = 0;
+    CUdevResource all; get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM);
+    const int want = getenv("BW_GREEN_SMS") ? atoi(getenv("BW_GREEN_SMS")) : 32;
+    std::vector<CUdevResource> pick;
+    if (gmode[0] == 's') {
+      unsigned n = all.sm.smCount / 8; std::vector<CUdevResource> grp(n); CUdevResource rest;
+      if (split(grp.data(), &n, &all, &rest, 0, 8) != CUDA_SUCCESS) { printf("split fail\n"); return 1; }
+      const unsigned k = want / 8;
+      for (unsigned i = 0; i < k; ++i) pick.push_back(grp[(2 * i + 1) * n / (2 * k)]);
+    } else {
+      unsigned n = 1; CUdevResource grp, rest;
+      if (split(&grp, &n, &all, &rest, 0, want) != CUDA_SUCCESS) { printf("split fail\n"); return 1; }
+      pick.push_back(grp);
+    }
+    CUdevResourceDesc d; CUgreenCtx g; CUstream st;
+    if (gen(&d, pick.data(), (unsigned)pick.size()) != CUDA_SUCCESS || create(&g, d, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        mkstream(&st, g, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) { printf("green ctx fail\n"); return 1; }
+    gstream = (cudaStream_t)st;
+  }
   struct Cfg { int mode, chunk, stages; };
   std::vector<Cfg> cfgs = {{1, 16384, 12}, {1, 4096, 48}, {1, 4096, 12}, {2, 16384, 12}, {2, 16384, 6}, {1, 32768, 6}};
   std::vector<int> sm_list = {16, 48, 148};
@@ -110,14 +145,15 @@ int main() {
       long long chunks = total_bytes / c.chunk;
       if (sms <= 16) chunks /= 8;
       int smem = c.stages * c.chunk + 1024;
-      stream_kernel<<<sms, 32, smem>>>(map, buf, c.mode, c.stages, c.chunk, chunks, rows);
-      CK(cudaEventRecord(e0));
-      for (int i = 0; i < 3; ++i) stream_kernel<<<sms, 32, smem>>>(map, buf, c.mode, c.stages, c.chunk, chunks, rows);
-      CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+      stream_kernel<<<sms, 32, smem, gstream>>>(map, buf, c.mode, c.stages, c.chunk, chunks, rows);
+      CK(cudaEventRecord(e0, gstream));
+      for (int i = 0; i < 3; ++i) stream_kernel<<<sms, 32, smem, gstream>>>(map, buf, c.mode, c.stages, c.chunk, chunks, rows);
+      CK(cudaEventRecord(e1, gstream)); CK(cudaEventSynchronize(e1));
       float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
       double gbs = 3.0 * chunks * c.chunk / (ms * 1e-3) / 1e9;
-      printf("{\"mode\": \"%s\", \"chunk\": %d, \"stages\": %d, \"sms\": %d, \"GBps\": %.0f, \"per_sm\": %.1f}\n",
-             c.mode == 2 ? "bulk4k_strided" : c.mode ? "bulk1d" : "tma2d", c.chunk, c.stages, sms, gbs, gbs / sms);
+      printf("{\"mode\": \"%s\", \"green\": \"%s\", \"chunk\": %d, \"stages\": %d, \"sms\": %d, \"GBps\": %.0f, \"per_sm\": %.1f}\n",
+             c.mode == 2 ? "bulk4k_strided" : c.mode ? "bulk1d" : "tma2d", gmode ? gmode : "none", c.chunk, c.stages, sms, gbs,
+             gbs / sms);
     }
   }
   return 0;
