@@ -540,6 +540,285 @@ __global__ void __launch_bounds__(2 * DecCfg<HP>::kPairs * 32, 1)
   }
 }
 
+// Page-wide decode attention (small lanes): item = sequence, all kv heads
+// of a page together. A dedicated producer warp streams each 16-token page
+// of the unit's tile range as ONE bulk copy of every kv head's block
+// ([page][kv head][K | V] is contiguous: Hkv x 8 KB, 64 KB at 8 kv heads)
+// into a 3-stage ring; consumer warp h owns kv head h (16 keys per stage)
+// and finalizes it alone. One issuing thread with 32-64 KB copies and
+// ~192 KB in flight is what a 32-SM lane needs to stream ~180 GB/s per SM
+// (profiles/r02_bw_probe_copy_size.jsonl, r02_bw_green.jsonl).
+constexpr int kPgStages = 3;
+template <int NH>
+struct PgCfg {
+  static constexpr int kStageBytes = NH * 8192;
+  static constexpr int kWarpStaging = 8 * kHD * 4;  // Q (bf16) at a segment's start, O (fp32) at its end
+  static constexpr size_t kSmem =
+      static_cast<size_t>(kPgStages) * kStageBytes + NH * kWarpStaging + 2 * kPgStages * 8 + 64;
+};
+static_assert(PgCfg<8>::kSmem <= 227u * 1024u, "page-wide decode ring exceeds 227 KB");
+
+template <int NH>
+__global__ void __launch_bounds__((NH + 1) * 32, 1)
+    decode_attn_page_kernel(AttnGeom g, const __nv_bfloat16* __restrict__ qkv,
+                            const __nv_bfloat16* __restrict__ kplane, const AttnSeq* __restrict__ seqs,
+                            const int* __restrict__ seq_prefix, int n_seq, long long total, long long W,
+                            const int32_t* __restrict__ pages, __nv_bfloat16* __restrict__ out,
+                            float* __restrict__ part_o, float* __restrict__ part_ml, int* __restrict__ item_done) {
+  extern __shared__ __align__(1024) uint8_t smem_pg[];
+  constexpr int kStage = PgCfg<NH>::kStageBytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem_pg;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_pg + kPgStages * kStage + NH * PgCfg<NH>::kWarpStaging);
+  uint64_t* empty = full + kPgStages;
+  pdl_trigger();
+  const long long gw = blockIdx.x;
+  if (gw >= W) return;  // the whole CTA leaves together
+  const long long lo = total * gw / W, hi = total * (gw + 1) / W;
+  if (warp == NH && lane == 0) {
+    for (int i = 0; i < kPgStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NH);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();  // the new token's K/V and Q come from the QKV / RoPE kernels
+  if (warp == NH) {
+    // ---------------- producer: one copy per page, all kv heads ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      DecPos prod = dec_locate(seq_prefix, n_seq, 1, lo);
+      int pm_seq = -1, kv_len = 0;
+      const int32_t* pt = pages;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = lo; t < hi; ++t) {
+        if (prod.seq != pm_seq) {
+          const AttnSeq ms = seqs[prod.seq];
+          pm_seq = prod.seq;
+          kv_len = ms.kv_len;
+          pt = pages + ms.page_off;
+        }
+        const int key = prod.tile * kKTD;  // < kv_len; a second page past it re-loads the first (masked)
+        const int pg0 = pt[key >> 4];
+        const int pg1 = key + 16 < kv_len ? pt[(key + 16) >> 4] : pg0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], kStage);
+          bulk_load(ring + stage * kStage, kplane + static_cast<size_t>(j ? pg1 : pg0) * NH * kKVBlock, kStage,
+                    &full[stage], pol);
+          if (++stage == kPgStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        dec_advance(prod, seq_prefix, n_seq, 1);
+      }
+    }
+    return;
+  }
+  // ---------------- consumer warp: kv head h ----------------
+  const int h = warp;
+  float* wstage = reinterpret_cast<float*>(smem_pg + kPgStages * kStage) + h * 8 * kHD;
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(wstage);
+  const uint32_t ring_s = smem_u32(ring) + static_cast<uint32_t>(h * 8192);
+  DecPos cur = dec_locate(seq_prefix, n_seq, 1, lo);
+  uint32_t qb[8][2];
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  float o[8][4];
+  AttnSeq meta = seqs[cur.seq];
+  int seg_tile0 = cur.tile;
+  const int h0 = 2 * (lane & 3);
+  const int l7 = lane & 7, b3 = (lane >> 3) & 1, b4 = lane >> 4, gx = (l7 & 6) >> 1;
+  uint32_t koff[4], voff[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    koff[j] = static_cast<uint32_t>(b3 * 2048 + l7 * 128 + (((b4 ^ l7) & 1) << 4) + ((j ^ gx) << 5));
+    voff[j] = static_cast<uint32_t>(4096 + b4 * 2048 + l7 * 128 + (((b3 ^ l7) & 1) << 4) + ((j ^ gx) << 5));
+  }
+  int stage = 0;
+  uint32_t phase = 0;
+  for (long long gt = lo; gt < hi; ++gt) {
+    if (gt == lo || cur.tile == 0) {  // new segment: this head's queries
+      meta = seqs[cur.seq];
+      seg_tile0 = cur.tile;
+      for (int c = lane; c < 8 * 16; c += 32) {
+        const int r = c >> 4, chunk = c & 15;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < g.group)
+          v = *reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(meta.q_start) * g.qkv_stride +
+                                              (h * g.group + r) * kHD + chunk * 8);
+        *reinterpret_cast<uint4*>(sq + r * kHD + ((chunk ^ (r & 7)) << 3)) = v;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        uint32_t r[4];
+        ldsm_x4(r, sq + swz(lane & 7, k * 16 + ((lane >> 3) << 3)));
+        qb[k][0] = r[0], qb[k][1] = r[1], qb[k + 1][0] = r[2], qb[k + 1][1] = r[3];
+      }
+      __syncwarp();  // the staging is the O staging at the segment's end
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t sbase = ring_s + static_cast<uint32_t>(stage * kStage);
+      float sc[4][4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sc[c][0] = sc[c][1] = sc[c][2] = sc[c][3] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t a[4];
+        ldsm_x4_s(a, sbase + koff[k & 3] + ((k & 4) << 8));
+        mma16816(sc[k & 3], a, qb[k][0], qb[k][1]);
+      }
+      float sv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sv[q] = (sc[0][q] + sc[1][q]) + (sc[2][q] + sc[3][q]);
+      const int key0 = cur.tile * kKTD + j * 16 + (lane >> 2);
+      float mx0 = m0, mx1 = m1;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const bool ok = key0 + q * 8 < meta.kv_len;
+        sv[2 * q] = ok ? sv[2 * q] * g.scale_log2 : -INFINITY;
+        sv[2 * q + 1] = ok ? sv[2 * q + 1] * g.scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, sv[2 * q]);
+        mx1 = fmaxf(mx1, sv[2 * q + 1]);
+      }
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, x));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, x));
+      }
+      const float bb0 = mx0 == -INFINITY ? 0.f : mx0, bb1 = mx1 == -INFINITY ? 0.f : mx1;
+      if (__any_sync(0xffffffff, mx0 != m0 || mx1 != m1)) {
+        const float al0 = ex2(m0 - bb0), al1 = ex2(m1 - bb1);
+        l0 *= al0, l1 *= al1;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) o[d][0] *= al0, o[d][2] *= al0, o[d][1] *= al1, o[d][3] *= al1;
+        m0 = mx0, m1 = mx1;
+      }
+      const float p00 = ex2(sv[0] - bb0), p01 = ex2(sv[1] - bb1);
+      const float p10 = ex2(sv[2] - bb0), p11 = ex2(sv[3] - bb1);
+      l0 += p00 + p10;
+      l1 += p01 + p11;
+      const uint32_t pb0 = movmatrix_trans(pack_bf16(p00, p01));
+      const uint32_t pb1 = movmatrix_trans(pack_bf16(p10, p11));
+#pragma unroll
+      for (int db = 0; db < 8; ++db) {
+        uint32_t a[4];
+        ldsm_x4_t_s(a, sbase + voff[db & 3] + ((db & 4) << 8));
+        mma16816(o[db], a, pb0, pb1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kPgStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    const bool item_end = cur.tile == cur.n_tiles - 1;
+    if (item_end || gt == hi - 1) {
+      float lt0 = l0, lt1 = l1;
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1) {
+        lt0 += __shfl_xor_sync(0xffffffff, lt0, x);
+        lt1 += __shfl_xor_sync(0xffffffff, lt1, x);
+      }
+      const bool whole = seg_tile0 == 0 && item_end;
+      const float sa0 = whole ? (lt0 > 0.f ? 1.f / lt0 : 0.f) : 1.f;
+      const float sa1 = whole ? (lt1 > 0.f ? 1.f / lt1 : 0.f) : 1.f;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        const int dim = d * 16 + (lane >> 2);
+        wstage[h0 * kHD + dim] = o[d][0] * sa0;
+        wstage[(h0 + 1) * kHD + dim] = o[d][1] * sa1;
+        wstage[h0 * kHD + dim + 8] = o[d][2] * sa0;
+        wstage[(h0 + 1) * kHD + dim + 8] = o[d][3] * sa1;
+      }
+      __syncwarp();
+      __nv_bfloat16* dst = out + static_cast<size_t>(meta.q_start) * g.out_stride + h * g.group * kHD;
+      if (whole) {
+        for (int c = lane; c < g.group * 16; c += 32) {
+          const float4 u = *reinterpret_cast<const float4*>(wstage + c * 8);
+          const float4 v = *reinterpret_cast<const float4*>(wstage + c * 8 + 4);
+          uint4 w;
+          w.x = pack_bf16(u.x, u.y), w.y = pack_bf16(u.z, u.w), w.z = pack_bf16(v.x, v.y), w.w = pack_bf16(v.z, v.w);
+          *reinterpret_cast<uint4*>(dst + c * 8) = w;
+        }
+      } else {
+        // partial slot (sequence + unit) x NH + head; the unit writing a
+        // head's last partial folds them (atomic count per (sequence, head))
+        const size_t slot = (static_cast<size_t>(cur.seq) + static_cast<size_t>(gw)) * NH + h;
+        float4* po = reinterpret_cast<float4*>(part_o + slot * g.group * kHD);
+        for (int c = lane; c < g.group * 32; c += 32) po[c] = *reinterpret_cast<const float4*>(wstage + c * 4);
+        if (lane < 4) {
+          if (h0 < g.group) {
+            part_ml[(slot * g.group + h0) * 2] = m0;
+            part_ml[(slot * g.group + h0) * 2 + 1] = lt0;
+          }
+          if (h0 + 1 < g.group) {
+            part_ml[(slot * g.group + h0 + 1) * 2] = m1;
+            part_ml[(slot * g.group + h0 + 1) * 2 + 1] = lt1;
+          }
+        }
+        __syncwarp();
+        const int item = cur.seq * NH + h;
+        const long long first = ((cur.item_start + 1) * W - 1) / total;
+        const long long lastu = ((cur.item_start + cur.n_tiles) * W - 1) / total;
+        const int pieces = static_cast<int>(lastu - first + 1);
+        int is_last = 0;
+        if (lane == 0) {
+          __threadfence();
+          is_last = atomicAdd(&item_done[item], 1) == pieces - 1;
+          if (is_last) item_done[item] = 0;
+        }
+        if (__shfl_sync(0xffffffffu, is_last, 0)) {
+          __threadfence();
+          const size_t base = static_cast<size_t>(cur.seq) + static_cast<size_t>(first);
+          for (int r = 0; r < g.group; ++r) {
+            float M = -INFINITY;
+            for (int q = lane; q < pieces; q += 32)
+              M = fmaxf(M, __ldcg(part_ml + (((base + q) * NH + h) * g.group + r) * 2));
+#pragma unroll
+            for (int x = 16; x > 0; x >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, x));
+            float L = 0.f;
+            for (int q = lane; q < pieces; q += 32) {
+              const size_t sl = ((base + q) * NH + h) * g.group + r;
+              const float ms = __ldcg(part_ml + sl * 2);
+              L += ms == -INFINITY ? 0.f : __ldcg(part_ml + sl * 2 + 1) * ex2(ms - M);
+            }
+#pragma unroll
+            for (int x = 16; x > 0; x >>= 1) L += __shfl_xor_sync(0xffffffffu, L, x);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+            for (int q = 0; q < pieces; ++q) {
+              const size_t sl = ((base + q) * NH + h) * g.group + r;
+              const float ms = __ldcg(part_ml + sl * 2);
+              const float4 o4 = __ldcg(reinterpret_cast<const float4*>(part_o + sl * kHD) + lane);
+              const float w = ms == -INFINITY ? 0.f : ex2(ms - M);
+              acc.x += o4.x * w, acc.y += o4.y * w, acc.z += o4.z * w, acc.w += o4.w * w;
+            }
+            const float inv = L > 0.f ? 1.f / L : 0.f;
+            uint2 pk;
+            pk.x = pack_bf16(acc.x * inv, acc.y * inv);
+            pk.y = pack_bf16(acc.z * inv, acc.w * inv);
+            *reinterpret_cast<uint2*>(dst + r * kHD + lane * 4) = pk;
+          }
+        }
+      }
+      __syncwarp();  // staging free for the next segment's Q
+    }
+    dec_advance(cur, seq_prefix, n_seq, 1);
+  }
+}
+
 // Items of HP kv heads: head pairs on lanes of >= 96 SMs when the kv-head
 // count is even (NX_DEC_HP=1 / 2 forces one form where it applies). Measured
 // (profiles/r02_attn_decode_variants_ab.jsonl, 8B): on the whole GPU head
@@ -567,6 +846,25 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (n_seq == 0 || total_tiles == 0) return cudaSuccess;
   if (g.group > 8) return cudaErrorInvalidValue;
   if (const cudaError_t pe = ensure_kernels_prepared(); pe != cudaSuccess) return pe;
+  // small lanes with 8 kv heads: page-wide items (one 64 KB copy per page);
+  // NX_DEC_PAGE=0 / 1 forces the choice where it applies
+  static const int page_force = [] {
+    const char* e = std::getenv("NX_DEC_PAGE");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (g.n_kv_heads == 8 && (page_force == 1 || (page_force < 0 && sm_count < 96))) {
+    static const long long kMinPg = [] {
+      const char* e = std::getenv("NX_DEC_MIN_TILES");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    const long long total_seq = total_tiles / 8;  // tiles per sequence (all heads in one item)
+    const long long Wp = std::min<long long>(sm_count, std::max<long long>(1, (total_seq + kMinPg - 1) / kMinPg));
+    if ((static_cast<size_t>(n_seq) + static_cast<size_t>(Wp)) * 8 * g.group * kHD > part_cap)
+      return cudaErrorInvalidValue;
+    ++g_kernel_launches;
+    return launch_pdl(decode_attn_page_kernel<8>, dim3(static_cast<int>(Wp)), dim3(9 * 32), PgCfg<8>::kSmem, s, g,
+                      qkv, kplane, seqs, seq_prefix, n_seq, total_seq, Wp, pages, out, part_o, part_ml, item_done);
+  }
   const int HP = decode_heads_per_item(g.n_kv_heads, sm_count);
   const int pairs = HP == 2 ? DecCfg<2>::kPairs : DecCfg<1>::kPairs;
   const size_t smem = HP == 2 ? DecCfg<2>::kSmem : DecCfg<1>::kSmem;
@@ -599,6 +897,9 @@ cudaError_t prepare_attention_kernels() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(decode_attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(DecCfg<2>::kSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(decode_attn_page_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(PgCfg<8>::kSmem));
   if (e == cudaSuccess) e = prepare_prefill_attention_kernel();
   return e;
 }
