@@ -846,24 +846,33 @@ cudaError_t decode_attention(const AttnGeom& g, const __nv_bfloat16* qkv,
   if (n_seq == 0 || total_tiles == 0) return cudaSuccess;
   if (g.group > 8) return cudaErrorInvalidValue;
   if (const cudaError_t pe = ensure_kernels_prepared(); pe != cudaSuccess) return pe;
-  // small lanes with 8 kv heads: page-wide items (one 64 KB copy per page);
-  // NX_DEC_PAGE=0 / 1 forces the choice where it applies
-  static const int page_force = [] {
+  // page-wide items (one copy of all kv heads per page) whenever the kv-head
+  // count is 2, 4 or 8: ahead of the pair kernels on every lane measured
+  // (profiles/r02_attn_decode_variants_ab.jsonl); NX_DEC_PAGE=0 turns it off
+  static const bool page_on = [] {
     const char* e = std::getenv("NX_DEC_PAGE");
-    return e ? std::atoi(e) : -1;
+    return !(e && e[0] == '0');
   }();
-  if (g.n_kv_heads == 8 && (page_force == 1 || (page_force < 0 && sm_count < 96))) {
+  const int nh = g.n_kv_heads;
+  if (page_on && (nh == 2 || nh == 4 || nh == 8)) {
     static const long long kMinPg = [] {
       const char* e = std::getenv("NX_DEC_MIN_TILES");
       return e ? std::max(1, std::atoi(e)) : 4;
     }();
-    const long long total_seq = total_tiles / 8;  // tiles per sequence (all heads in one item)
+    const long long total_seq = total_tiles / nh;  // tiles per sequence (all heads in one item)
     const long long Wp = std::min<long long>(sm_count, std::max<long long>(1, (total_seq + kMinPg - 1) / kMinPg));
-    if ((static_cast<size_t>(n_seq) + static_cast<size_t>(Wp)) * 8 * g.group * kHD > part_cap)
+    if ((static_cast<size_t>(n_seq) + static_cast<size_t>(Wp)) * nh * g.group * kHD > part_cap)
       return cudaErrorInvalidValue;
     ++g_kernel_launches;
-    return launch_pdl(decode_attn_page_kernel<8>, dim3(static_cast<int>(Wp)), dim3(9 * 32), PgCfg<8>::kSmem, s, g,
-                      qkv, kplane, seqs, seq_prefix, n_seq, total_seq, Wp, pages, out, part_o, part_ml, item_done);
+    const dim3 grid_p(static_cast<int>(Wp)), block_p((nh + 1) * 32);
+    if (nh == 8)
+      return launch_pdl(decode_attn_page_kernel<8>, grid_p, block_p, PgCfg<8>::kSmem, s, g, qkv, kplane, seqs,
+                        seq_prefix, n_seq, total_seq, Wp, pages, out, part_o, part_ml, item_done);
+    if (nh == 4)
+      return launch_pdl(decode_attn_page_kernel<4>, grid_p, block_p, PgCfg<4>::kSmem, s, g, qkv, kplane, seqs,
+                        seq_prefix, n_seq, total_seq, Wp, pages, out, part_o, part_ml, item_done);
+    return launch_pdl(decode_attn_page_kernel<2>, grid_p, block_p, PgCfg<2>::kSmem, s, g, qkv, kplane, seqs,
+                      seq_prefix, n_seq, total_seq, Wp, pages, out, part_o, part_ml, item_done);
   }
   const int HP = decode_heads_per_item(g.n_kv_heads, sm_count);
   const int pairs = HP == 2 ? DecCfg<2>::kPairs : DecCfg<1>::kPairs;
@@ -900,6 +909,12 @@ cudaError_t prepare_attention_kernels() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(decode_attn_page_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(PgCfg<8>::kSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(decode_attn_page_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(PgCfg<4>::kSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(decode_attn_page_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(PgCfg<2>::kSmem));
   if (e == cudaSuccess) e = prepare_prefill_attention_kernel();
   return e;
 }
