@@ -647,8 +647,9 @@ def run_bench(args, rank, world, local, dist, nx, D, np, dev, tp, tp_nccl, num_p
         "same_kernel_baselines": baselines,
         # not measured in this run: the paper's throughput metric from tools/capacity.py (3 held-out seeds x
         # 2,000 requests per probe, >= 90% of requests inside both SLOs), same defaults as this line
-        "capacity_rps_reference": {"source": "profiles/r02_capacity_8b_tuned_seeds301.json",
-                                   "nexus": 125.0, "monolithic": 119.0} if args.model == "llama3-8b" else None,
+        "capacity_rps_reference": {"source": ["profiles/r02_capacity_8b_refit_seeds301.json",
+                                              "profiles/r02_capacity_8b_mono_page_seeds301.json"],
+                                   "nexus": 124.0, "monolithic": 119.0} if args.model == "llama3-8b" else None,
         "decisions": sum(r["decisions"] for r in results), "switches": sum(r["switches"] for r in results),
         "r_p_hist_arrivals": {str(k): sum(r["r_p_hist"].get(k, 0) for r in results)
                               for k in sorted({k for r in results for k in r["r_p_hist"]})},
