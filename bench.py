@@ -90,7 +90,7 @@ def parse():
     p.add_argument("--beta", type=float, default=1.5,
                    help="ControllerConfig.beta, the decode slack in prefill-prioritized mode (paper 1.1, set for "
                         "L20). 1.5 with decode batch 256 keeps decode steps short enough that a request's first "
-                        "decode gap stays inside the TBT SLO (capacity 125 vs 119 rps for the monolithic "
+                        "decode gap stays inside the TBT SLO (capacity 124 vs 119 rps for the monolithic "
                         "baseline on held-out seeds, profiles/r02_summary.md); 2.0 was round 1's default")
     p.add_argument("--gamma", type=float, default=None,
                    help="ControllerConfig.gamma (SPF aging, tokens of priority per second waited; reference "
